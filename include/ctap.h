@@ -1,0 +1,159 @@
+/*
+ * ctap.h -- C ABI of libctap.so, the B200 (sm_100a) split-step Fourier
+ * propagator for the 3D time-dependent Schrodinger equation on the CTAP
+ * atom-chip grid.
+ *
+ * The reference (arXiv:1309.2451, package `ctapsim`) is pure Python and has
+ * no FFI; each entry point below replaces one reference function and is what
+ * its Python host layer (paper_1309_2451_b200/, or a ctypes stub inside
+ * ctapsim itself) binds.  Reference paths are relative to
+ * /root/reference/pkg/src/ctapsim/.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Device pointers are CUDA global memory
+ *     owned by the caller; `stream` is a cudaStream_t (NULL = legacy stream).
+ *     All work is stream-ordered; nothing synchronises the host unless noted.
+ *   - Wavefunctions are complex128 interleaved (re, im), C order (nx, ny, nz)
+ *     with z fastest (qgrid.py:3-7).  Potentials are float64 in joules.
+ *   - Every call returns a ctap_status; ctap_last_error() gives a thread-local
+ *     message for the last failure on the calling thread.
+ *   - A plan is not thread safe: one driver thread per plan (propagator.py:136-142).
+ *   - Slab decomposition: with slab_p > 1 the plan describes rank slab_r of
+ *     slab_p x-slabs (nx/slab_p x-planes each); the caller moves data between
+ *     ranks (NCCL all-to-all) between the passes, see ctap_pass().
+ */
+#ifndef CTAP_H
+#define CTAP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CTAP_API __attribute__((visibility("default")))
+
+typedef enum ctap_status {
+  CTAP_OK = 0,
+  CTAP_EINVAL = 1,       /* invalid argument (reference raises ValueError) */
+  CTAP_ECUDA = 2,        /* CUDA runtime error */
+  CTAP_EUNSUPPORTED = 3, /* shape outside the compiled kernel set */
+  CTAP_ENOMEM = 4
+} ctap_status;
+
+typedef enum ctap_mode {
+  CTAP_REAL_TIME = 0,      /* propagator.REAL_TIME */
+  CTAP_IMAGINARY_TIME = 1  /* propagator.IMAGINARY_TIME */
+} ctap_mode;
+
+/* Axis passes. */
+typedef enum ctap_pass_kind {
+  CTAP_PASS_Z_FWD = 0,
+  CTAP_PASS_Z_INV = 1,
+  CTAP_PASS_Z_FIRST = 2,  /* psi <- Fz (Vh psi)             segment start */
+  CTAP_PASS_Z_MID = 3,    /* psi <- Fz V Fz^-1 psi          between steps */
+  CTAP_PASS_Z_LAST = 4,   /* psi <- Vh Fz^-1 psi            segment end   */
+  CTAP_PASS_Y_FWD = 5,
+  CTAP_PASS_Y_INV = 6,
+  CTAP_PASS_Y_FWD_TO_PEER = 7,   /* y FFT, output in peer-major send layout */
+  CTAP_PASS_Y_INV_FROM_PEER = 8, /* input in peer-major receive layout, y^-1 */
+  CTAP_PASS_X_KIN = 9,    /* psi <- Fx^-1 (K/N) Fx psi on the y-slab layout */
+  CTAP_PASS_X_FWD = 10,
+  CTAP_PASS_X_INV = 11
+} ctap_pass_kind;
+
+typedef struct ctap_plan ctap_plan;
+
+/* Scalars of make_plan (propagator.py:55-81), computed by the host exactly as
+ * the reference computes them:
+ *   e0   = UnitSystem.energy  = hbar**2 / (mass * 1e-6**2)      (qgrid.py:41-43)
+ *   dt_i = dt / UnitSystem.time, time = mass * 1e-6**2 / hbar   (qgrid.py:37-39)
+ *   len2 = UnitSystem.length**2 (1e-12)
+ *   v_shift = 0 in real time, potential.min() in imaginary time (propagator.py:75) */
+typedef struct ctap_plan_desc {
+  int64_t n[3];     /* global nx, ny, nz: powers of two in [8, 1024] */
+  double e0;
+  double dt_i;
+  double len2;
+  double v_shift;
+  int32_t mode;     /* ctap_mode */
+  int32_t slab_p;   /* number of x-slab ranks (1 = single GPU) */
+  int32_t slab_r;   /* this rank */
+  int32_t reserved;
+} ctap_plan_desc;
+
+/* make_plan (propagator.py:55-81).  kx2/ky2/kz2 are HOST arrays of the squared
+ * angular wavenumbers k_axis(i)**2 in m^-2 (qgrid.py:98-117), full global
+ * length.  v_dev is the caller's device potential slab (nx/slab_p, ny, nz),
+ * which must stay alive for the plan's lifetime.  The phase factors are never
+ * materialised: they are recomputed per point with the reference's exact
+ * operation order inside the passes. */
+CTAP_API int ctap_plan_create(const ctap_plan_desc* desc, const double* kx2, const double* ky2,
+                              const double* kz2, const double* v_dev, ctap_plan** out);
+CTAP_API int ctap_plan_destroy(ctap_plan* plan);
+
+/* _advance (propagator.py:98-107): n telescoped Strang steps in place on the
+ * device wavefunction (single-GPU plans only; slab plans use ctap_pass).
+ * n_steps == 0 leaves psi untouched. */
+CTAP_API int ctap_advance(ctap_plan* plan, void* psi_dev, int64_t n_steps, void* stream);
+
+/* One axis pass (the building block of ctap_advance, exposed for the slab
+ * decomposition and the plain 3D FFT of kinetic_expectation). z passes are in
+ * place (in == out).  Y/X passes may be in place in the natural layout. */
+CTAP_API int ctap_pass(ctap_plan* plan, int32_t pass_kind, const void* in_dev, void* out_dev,
+                       void* stream);
+
+/* Observer reductions (observables.py:74-110, qgrid.py:150-154) over the local
+ * slab in one read of psi.  out_dev[5] (device) receives the raw sums
+ *   [ sum |psi|^2, sum_{x<xb1(z)} |psi|^2, sum_middle, sum_{x>=xb2(z)}, sum_edge ]
+ * where the edge set is every cell within `margin` cells of a global face.
+ * xs_dev: local x axis values (m); xb1_dev/xb2_dev: partition boundaries per z
+ * (may be NULL: populations are then reported as 0).  The caller scales by
+ * dx*dy*dz exactly like the reference.  Deterministic (fixed-order tree). */
+CTAP_API int ctap_observe(ctap_plan* plan, const void* psi_dev, const double* xs_dev,
+                          const double* xb1_dev, const double* xb2_dev, int32_t margin,
+                          double* out_dev, void* stream);
+
+/* density_xz (observables.py:91-94) raw sums: out_dev[x][z] = sum_y |psi|^2
+ * over the local slab (nx/slab_p, nz). */
+CTAP_API int ctap_density_xz(ctap_plan* plan, const void* psi_dev, double* out_dev, void* stream);
+
+/* Reductions of energy_expectation (propagator.py:176-195).
+ * ctap_k2_sums: on a momentum-space array in the y-slab layout (x, y_local, z)
+ *   out_dev[2] = [ sum k^2 |phi|^2 (m^-2), sum |phi|^2 ].
+ * ctap_v_sums: on position space, out_dev[2] = [ sum V |psi|^2, sum |psi|^2 ]. */
+CTAP_API int ctap_k2_sums(ctap_plan* plan, const void* phi_dev, double* out_dev, void* stream);
+CTAP_API int ctap_v_sums(ctap_plan* plan, const void* psi_dev, double* out_dev, void* stream);
+
+/* StepPlan.exp_v_half / exp_v_full / exp_k (propagator.py:45-47, 65-68,
+ * 76-78) materialised on the local slab for inspection (which = 0, 1, 2):
+ * complex128 cos(phi) + i sin(phi) in real time, exp(phi) + 0i in imaginary
+ * time.  The propagation never stores these fields. */
+CTAP_API int ctap_phase_field(ctap_plan* plan, int32_t which, void* out_dev, void* stream);
+
+/* Wavefunction.normalize (qgrid.py:159-162): psi /= divisor (IEEE division). */
+CTAP_API int ctap_scale(ctap_plan* plan, void* psi_dev, double divisor, void* stream);
+
+/* Single-GPU forward (direction -1) or inverse-unnormalised (+1) 3D FFT in
+ * place, as scipy.fft.fftn in kinetic_expectation (propagator.py:181). */
+CTAP_API int ctap_fft3d(ctap_plan* plan, void* data_dev, int32_t direction, void* stream);
+
+/* _potential_kernel (magfield.py:107-144): V on the (local) grid, float64,
+ * bit-identical to the reference's IEEE sequential evaluation (segments in
+ * order, no FMA contraction).  All arrays are device pointers: xs (nx), ys
+ * (ny), zs (nz) axis samples; seg_a/seg_b (n_seg x 3, row major) segment
+ * end points; seg_cur (n_seg) currents.  V_out has shape (nx, ny, nz). */
+CTAP_API int ctap_potential(const double* xs, int64_t nx, const double* ys, int64_t ny,
+                            const double* zs, int64_t nz, const double* seg_a, const double* seg_b,
+                            const double* seg_cur, int64_t n_seg, double b0x, double b0y, double b0z,
+                            double mu_eff, double mass, double omega_z, double z_center,
+                            double pref, double* V_out, void* stream);
+
+CTAP_API const char* ctap_last_error(void);
+CTAP_API const char* ctap_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CTAP_H */

@@ -1,0 +1,225 @@
+// C ABI of libctap.so (include/ctap.h): plan lifetime, error reporting and
+// the per-segment driver loop that replaces propagator._advance.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ctap_internal.h"
+
+cudaError_t ctap_run_observe(const ctap_plan* p, const void* psi, const double* xs, const double* xb1,
+                             const double* xb2, int margin, double* out, cudaStream_t st);
+cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, cudaStream_t st);
+cudaError_t ctap_run_v_sums(const ctap_plan* p, const void* psi, double* out, cudaStream_t st);
+cudaError_t ctap_run_density_xz(const ctap_plan* p, const void* psi, double* out, cudaStream_t st);
+cudaError_t ctap_run_phase_field(const ctap_plan* p, int which, void* out, cudaStream_t st);
+cudaError_t ctap_run_scale(const ctap_plan* p, void* psi, double d, cudaStream_t st);
+cudaError_t ctap_run_potential(const double* xs, int64_t nx, const double* ys, int64_t ny, const double* zs,
+                               int64_t nz, const double* seg_a, const double* seg_b, const double* seg_cur,
+                               int64_t n_seg, double b0x, double b0y, double b0z, double mu_eff, double mass,
+                               double omega_z, double z_center, double pref, double* V_out, cudaStream_t st);
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(CTAP_ECUDA, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+bool pow2_in_range(int64_t n) { return n >= 8 && n <= 1024 && (n & (n - 1)) == 0; }
+
+// exp(-2 pi i m / L) for L = 8..1024, concatenated (table for L at offset L-8),
+// evaluated in extended precision so every entry is the correctly rounded
+// double (the FFT round-off budget relies on ~1-ulp twiddles).
+std::vector<double> make_twiddles() {
+  std::vector<double> t;
+  for (int L = 8; L <= 1024; L *= 2) {
+    for (int m = 0; m < L; ++m) {
+      long double ang = 2.0L * 3.14159265358979323846264338327950288L * (long double)m / (long double)L;
+      t.push_back((double)cosl(ang));
+      t.push_back((double)(-sinl(ang)));
+    }
+  }
+  return t;
+}
+
+}  // namespace
+
+#define CUDA_TRY(expr, what)                       \
+  do {                                             \
+    cudaError_t e_ = (expr);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+extern "C" {
+
+CTAP_API const char* ctap_last_error(void) { return g_err.c_str(); }
+CTAP_API const char* ctap_version(void) { return "ctap 0.1.0 (sm_100a)"; }
+
+CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const double* ky2, const double* kz2,
+                              const double* v_dev, ctap_plan** out) {
+  if (!d || !out || !kx2 || !ky2 || !kz2) return fail(CTAP_EINVAL, "null argument");
+  *out = nullptr;
+  for (int i = 0; i < 3; ++i)
+    if (!pow2_in_range(d->n[i]))
+      return fail(CTAP_EUNSUPPORTED, "grid counts must be powers of two in [8, 1024], got %lld",
+                  (long long)d->n[i]);
+  if (d->mode != CTAP_REAL_TIME && d->mode != CTAP_IMAGINARY_TIME)
+    return fail(CTAP_EINVAL, "unknown mode %d", d->mode);
+  int P = d->slab_p < 1 ? 1 : d->slab_p;
+  if (d->n[0] % P || d->n[1] % P) return fail(CTAP_EINVAL, "nx and ny must be divisible by the %d slab ranks", P);
+  if (d->slab_r < 0 || d->slab_r >= P) return fail(CTAP_EINVAL, "slab rank %d out of range", d->slab_r);
+  if (!v_dev) return fail(CTAP_EINVAL, "potential pointer is null");
+
+  ctap_plan* p = new ctap_plan();
+  std::memset(p, 0, sizeof *p);
+  for (int i = 0; i < 3; ++i) p->n[i] = d->n[i];
+  p->slab_p = P;
+  p->slab_r = d->slab_r;
+  p->nx_local = d->n[0] / P;
+  p->mode = d->mode;
+  p->e0 = d->e0;
+  p->dt_i = d->dt_i;
+  p->len2 = d->len2;
+  p->v_shift = d->v_shift;
+  p->v_dev = v_dev;
+  p->inv_scale = 1.0 / (double)(d->n[0] * d->n[1] * d->n[2]);  // exact: power of two
+  const double* k2h[3] = {kx2, ky2, kz2};
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+    e = cudaMalloc((void**)&p->k2_dev[i], sizeof(double) * d->n[i]);
+    if (e == cudaSuccess) e = cudaMemcpy(p->k2_dev[i], k2h[i], sizeof(double) * d->n[i], cudaMemcpyHostToDevice);
+  }
+  std::vector<double> tw = make_twiddles();
+  if (e == cudaSuccess) e = cudaMalloc((void**)&p->twiddles, tw.size() * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(p->twiddles, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice);
+  int dev = 0, sms = 148;
+  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  p->red_blocks = sms * 4;
+  if (e == cudaSuccess) e = cudaMalloc((void**)&p->red_partial, sizeof(double) * 8 * p->red_blocks);
+  if (e != cudaSuccess) {
+    ctap_plan_destroy(p);
+    return cuda_fail(e, "ctap_plan_create");
+  }
+  *out = p;
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_plan_destroy(ctap_plan* p) {
+  if (!p) return CTAP_OK;
+  for (int i = 0; i < 3; ++i) cudaFree(p->k2_dev[i]);
+  cudaFree(p->twiddles);
+  cudaFree(p->red_partial);
+  delete p;
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, void* stream) {
+  if (!p || !in || !out) return fail(CTAP_EINVAL, "null argument");
+  if (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_X_INV) return fail(CTAP_EINVAL, "unknown pass %d", kind);
+  if (kind <= CTAP_PASS_Z_LAST && in != out) return fail(CTAP_EINVAL, "z passes run in place");
+  CUDA_TRY(ctap_run_pass(p, kind, in, out, (cudaStream_t)stream), "ctap_pass");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
+  if (!p || !psi) return fail(CTAP_EINVAL, "null argument");
+  if (n < 0) return fail(CTAP_EINVAL, "n_steps must be >= 0");
+  if (p->slab_p != 1) return fail(CTAP_EINVAL, "ctap_advance drives single-GPU plans; use ctap_pass for slabs");
+  if (n == 0) return CTAP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Z_FIRST, psi, psi, st), "ctap_advance");
+  for (int64_t j = 0; j < n; ++j) {
+    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Y_FWD, psi, psi, st), "ctap_advance");
+    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, st), "ctap_advance");
+    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Y_INV, psi, psi, st), "ctap_advance");
+    CUDA_TRY(ctap_run_pass(p, j < n - 1 ? CTAP_PASS_Z_MID : CTAP_PASS_Z_LAST, psi, psi, st), "ctap_advance");
+  }
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_fft3d(ctap_plan* p, void* data, int32_t direction, void* stream) {
+  if (!p || !data) return fail(CTAP_EINVAL, "null argument");
+  if (p->slab_p != 1) return fail(CTAP_EINVAL, "ctap_fft3d is single-GPU; slab plans compose ctap_pass");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (direction < 0) {
+    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Z_FWD, data, data, st), "ctap_fft3d");
+    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Y_FWD, data, data, st), "ctap_fft3d");
+    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_X_FWD, data, data, st), "ctap_fft3d");
+  } else {
+    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_X_INV, data, data, st), "ctap_fft3d");
+    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Y_INV, data, data, st), "ctap_fft3d");
+    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Z_INV, data, data, st), "ctap_fft3d");
+  }
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_observe(ctap_plan* p, const void* psi, const double* xs, const double* xb1, const double* xb2,
+                          int32_t margin, double* out, void* stream) {
+  if (!p || !psi || !out || !xs) return fail(CTAP_EINVAL, "null argument");
+  if ((xb1 == nullptr) != (xb2 == nullptr)) return fail(CTAP_EINVAL, "xb1 and xb2 must both be given");
+  if (margin < 1) return fail(CTAP_EINVAL, "margin_cells must be >= 1");
+  CUDA_TRY(ctap_run_observe(p, psi, xs, xb1, xb2, margin, out, (cudaStream_t)stream), "ctap_observe");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_density_xz(ctap_plan* p, const void* psi, double* out, void* stream) {
+  if (!p || !psi || !out) return fail(CTAP_EINVAL, "null argument");
+  CUDA_TRY(ctap_run_density_xz(p, psi, out, (cudaStream_t)stream), "ctap_density_xz");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_k2_sums(ctap_plan* p, const void* phi, double* out, void* stream) {
+  if (!p || !phi || !out) return fail(CTAP_EINVAL, "null argument");
+  CUDA_TRY(ctap_run_k2_sums(p, phi, out, (cudaStream_t)stream), "ctap_k2_sums");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_v_sums(ctap_plan* p, const void* psi, double* out, void* stream) {
+  if (!p || !psi || !out) return fail(CTAP_EINVAL, "null argument");
+  CUDA_TRY(ctap_run_v_sums(p, psi, out, (cudaStream_t)stream), "ctap_v_sums");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_phase_field(ctap_plan* p, int32_t which, void* out, void* stream) {
+  if (!p || !out) return fail(CTAP_EINVAL, "null argument");
+  if (which < 0 || which > 2) return fail(CTAP_EINVAL, "which must be 0 (v_half), 1 (v_full) or 2 (k)");
+  CUDA_TRY(ctap_run_phase_field(p, which, out, (cudaStream_t)stream), "ctap_phase_field");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_scale(ctap_plan* p, void* psi, double divisor, void* stream) {
+  if (!p || !psi) return fail(CTAP_EINVAL, "null argument");
+  if (!(divisor > 0.0) || !std::isfinite(divisor)) return fail(CTAP_EINVAL, "divisor must be positive and finite");
+  CUDA_TRY(ctap_run_scale(p, psi, divisor, (cudaStream_t)stream), "ctap_scale");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_potential(const double* xs, int64_t nx, const double* ys, int64_t ny, const double* zs, int64_t nz,
+                            const double* seg_a, const double* seg_b, const double* seg_cur, int64_t n_seg,
+                            double b0x, double b0y, double b0z, double mu_eff, double mass, double omega_z,
+                            double z_center, double pref, double* V_out, void* stream) {
+  if (!xs || !ys || !zs || !V_out) return fail(CTAP_EINVAL, "null argument");
+  if (n_seg < 0 || (n_seg > 0 && (!seg_a || !seg_b || !seg_cur))) return fail(CTAP_EINVAL, "bad segment arrays");
+  if (nx <= 0 || ny <= 0 || nz <= 0) return fail(CTAP_EINVAL, "empty grid");
+  CUDA_TRY(ctap_run_potential(xs, nx, ys, ny, zs, nz, seg_a, seg_b, seg_cur, n_seg, b0x, b0y, b0z, mu_eff, mass,
+                              omega_z, z_center, pref, V_out, (cudaStream_t)stream),
+           "ctap_potential");
+  return CTAP_OK;
+}
+
+}  // extern "C"

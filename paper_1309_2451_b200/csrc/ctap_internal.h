@@ -1,0 +1,47 @@
+// Internal plan object shared by the kernels and the C ABI (not exported).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ctap.h"
+
+namespace ctap {
+enum PassKind {
+  // z passes (contiguous lines, always in place)
+  PASS_Z_FWD = CTAP_PASS_Z_FWD,
+  PASS_Z_INV = CTAP_PASS_Z_INV,
+  PASS_Z_FIRST = CTAP_PASS_Z_FIRST,  // Vh, then Fz
+  PASS_Z_MID = CTAP_PASS_Z_MID,      // Fz^-1, V, Fz
+  PASS_Z_LAST = CTAP_PASS_Z_LAST,    // Fz^-1, then Vh
+  // y passes
+  PASS_Y_FWD = CTAP_PASS_Y_FWD,
+  PASS_Y_INV = CTAP_PASS_Y_INV,
+  PASS_Y_FWD_TO_PEER = CTAP_PASS_Y_FWD_TO_PEER,
+  PASS_Y_INV_FROM_PEER = CTAP_PASS_Y_INV_FROM_PEER,
+  // x passes (y-slab layout)
+  PASS_X_KIN = CTAP_PASS_X_KIN,  // Fx, K / N, Fx^-1
+  PASS_X_FWD = CTAP_PASS_X_FWD,
+  PASS_X_INV = CTAP_PASS_X_INV,
+  // strided kernel variants
+  PASS_S_FWD = 100,
+  PASS_S_INV = 101,
+  PASS_S_KIN = 102,
+};
+}  // namespace ctap
+
+struct ctap_plan {
+  int64_t n[3];
+  int64_t nx_local;
+  int slab_p, slab_r;
+  int mode;  // 0 real, 1 imaginary
+  double e0, dt_i, len2, v_shift;
+  double inv_scale;        // 1 / (nx ny nz), exact power of two
+  const double* v_dev;     // caller-owned potential slab
+  double* k2_dev[3];       // squared wavenumbers per axis (global lengths)
+  double2* twiddles;       // concatenated exp(-2 pi i m / L), L = 8..1024
+  double* red_partial;     // reduction scratch
+  int red_blocks;
+};
+
+cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* out, cudaStream_t st);

@@ -1,0 +1,203 @@
+// Deterministic reductions over |psi|^2: observer sums (norm, guide
+// populations, edge mass), energy sums, the y-integrated density map and the
+// normalisation scale.  Reference: observables.py:74-110, qgrid.py:150-162,
+// propagator.py:176-195.
+//
+// Every reduction is two fixed-shape stages (grid-stride partial sums per
+// block in a fixed order, then one block summing the partials in a fixed
+// tree), so results are bitwise reproducible run to run with no float atomics
+// (reference determinism rule: test_propagator.py:147-154).
+#include "ctap_device.cuh"
+#include "ctap_internal.h"
+
+namespace ctap {
+
+constexpr int kRedThreads = 256;
+
+template <int NV>
+__device__ __forceinline__ void block_reduce_store(double (&acc)[NV], double* __restrict__ out) {
+  __shared__ double sh[NV][kRedThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[k][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kRedThreads / 32; ++w) s += sh[threadIdx.x][w];
+    out[threadIdx.x] = s;
+  }
+}
+
+template <int NV, typename F>
+__global__ void __launch_bounds__(kRedThreads) reduce_kernel(F f, int64_t n, double* __restrict__ partial) {
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f(i, acc);
+  block_reduce_store<NV>(acc, partial + (size_t)blockIdx.x * NV);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(kRedThreads) finalize_kernel(const double* __restrict__ partial, int nblocks,
+                                                               double* __restrict__ out) {
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] += partial[(size_t)b * NV + k];
+  }
+  block_reduce_store<NV>(acc, out);
+}
+
+struct ObserveF {
+  const double2* psi;
+  const double* xs;
+  const double* xb1;
+  const double* xb2;
+  int64_t nyz, ny, nz, nx_global, x_off;
+  int margin;
+  __device__ __forceinline__ void operator()(int64_t i, double (&acc)[5]) const {
+    double2 a = psi[i];
+    double rho = a.x * a.x + a.y * a.y;
+    int64_t x = i / nyz;
+    int64_t r = i - x * nyz;
+    int64_t y = r / nz;
+    int64_t z = r - y * nz;
+    acc[0] += rho;
+    if (xb1 != nullptr) {
+      double xv = xs[x];
+      bool in_l = xv < xb1[z];
+      bool in_r = xv >= xb2[z];
+      if (in_l) acc[1] += rho;
+      if (in_r) acc[3] += rho;
+      if (!(in_l || in_r)) acc[2] += rho;
+    }
+    int64_t gx = x + x_off;
+    bool edge = gx < margin || gx >= nx_global - margin || y < margin || y >= ny - margin || z < margin ||
+                z >= nz - margin;
+    if (edge) acc[4] += rho;
+  }
+};
+
+struct K2F {
+  const double2* phi;
+  const double* kx2;
+  const double* ky2;
+  const double* kz2;
+  int64_t nylz, nyl, nz, y_off;
+  __device__ __forceinline__ void operator()(int64_t i, double (&acc)[2]) const {
+    double2 a = phi[i];
+    double rho = a.x * a.x + a.y * a.y;
+    int64_t x = i / nylz;
+    int64_t r = i - x * nylz;
+    int64_t y = r / nz;
+    int64_t z = r - y * nz;
+    double k2 = (kx2[x] + ky2[y + y_off]) + kz2[z];
+    acc[0] += k2 * rho;
+    acc[1] += rho;
+  }
+};
+
+struct VF {
+  const double2* psi;
+  const double* V;
+  __device__ __forceinline__ void operator()(int64_t i, double (&acc)[2]) const {
+    double2 a = psi[i];
+    double rho = a.x * a.x + a.y * a.y;
+    acc[0] += V[i] * rho;
+    acc[1] += rho;
+  }
+};
+
+template <int NV, typename F>
+static cudaError_t run_reduce(const ctap_plan* p, F f, int64_t n, double* out, cudaStream_t st) {
+  reduce_kernel<NV><<<p->red_blocks, kRedThreads, 0, st>>>(f, n, p->red_partial);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  finalize_kernel<NV><<<1, kRedThreads, 0, st>>>(p->red_partial, p->red_blocks, out);
+  return cudaGetLastError();
+}
+
+__global__ void density_xz_kernel(const double2* __restrict__ psi, int64_t nxl, int64_t ny, int64_t nz,
+                                  double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nxl * nz) return;
+  int64_t x = i / nz, z = i - (i / nz) * nz;
+  const double2* base = psi + x * ny * nz + z;
+  double s = 0.0;
+  for (int64_t y = 0; y < ny; ++y) {
+    double2 a = base[y * nz];
+    s += a.x * a.x + a.y * a.y;
+  }
+  out[i] = s;
+}
+
+__global__ void scale_kernel(double2* __restrict__ psi, int64_t n, double d) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double2 a = psi[i];
+    psi[i] = make_double2(a.x / d, a.y / d);
+  }
+}
+
+}  // namespace ctap
+
+using namespace ctap;
+
+cudaError_t ctap_run_observe(const ctap_plan* p, const void* psi, const double* xs, const double* xb1,
+                             const double* xb2, int margin, double* out, cudaStream_t st) {
+  ObserveF f;
+  f.psi = (const double2*)psi;
+  f.xs = xs;
+  f.xb1 = xb1;
+  f.xb2 = xb2;
+  f.nyz = p->n[1] * p->n[2];
+  f.ny = p->n[1];
+  f.nz = p->n[2];
+  f.nx_global = p->n[0];
+  f.x_off = (int64_t)p->slab_r * p->nx_local;
+  f.margin = margin;
+  return run_reduce<5>(p, f, p->nx_local * f.nyz, out, st);
+}
+
+cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, cudaStream_t st) {
+  K2F f;
+  f.phi = (const double2*)phi;
+  f.kx2 = p->k2_dev[0];
+  f.ky2 = p->k2_dev[1];
+  f.kz2 = p->k2_dev[2];
+  f.nyl = p->n[1] / p->slab_p;
+  f.nz = p->n[2];
+  f.nylz = f.nyl * f.nz;
+  f.y_off = (int64_t)p->slab_r * f.nyl;
+  return run_reduce<2>(p, f, p->n[0] * f.nylz, out, st);
+}
+
+cudaError_t ctap_run_v_sums(const ctap_plan* p, const void* psi, double* out, cudaStream_t st) {
+  VF f;
+  f.psi = (const double2*)psi;
+  f.V = p->v_dev;
+  return run_reduce<2>(p, f, p->nx_local * p->n[1] * p->n[2], out, st);
+}
+
+cudaError_t ctap_run_density_xz(const ctap_plan* p, const void* psi, double* out, cudaStream_t st) {
+  int64_t n = p->nx_local * p->n[2];
+  int threads = 256;
+  density_xz_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, st>>>(
+      (const double2*)psi, p->nx_local, p->n[1], p->n[2], out);
+  return cudaGetLastError();
+}
+
+cudaError_t ctap_run_scale(const ctap_plan* p, void* psi, double d, cudaStream_t st) {
+  int64_t n = p->nx_local * p->n[1] * p->n[2];
+  scale_kernel<<<p->red_blocks, kRedThreads, 0, st>>>((double2*)psi, n, d);
+  return cudaGetLastError();
+}

@@ -1,0 +1,64 @@
+"""Per-pass device timing (CUDA events) of the split-step passes on one GPU.
+
+usage: python scripts/pass_timing.py NX NY NZ [reps]
+Prints ms per pass and the achieved GB/s against 32 B/pt (+8 B/pt V for z
+passes with a potential phase).
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+
+from paper_1309_2451_b200 import _lib, propagator, qgrid
+from paper_1309_2451_b200.constants import muB, species_mass
+
+
+def main():
+    nx, ny, nz = (int(v) for v in sys.argv[1:4])
+    reps = int(sys.argv[4]) if len(sys.argv) > 4 else 20
+    m = species_mass("li6")
+    grid = qgrid.make_grid(nx, ny, nz, (20e-6, 4e-6, 1000e-6), origin=(-10e-6, 4e-6 / ny / 2, 0.0))
+    n = nx * ny * nz
+    v = torch.full((nx, ny, nz), muB / 2 * 0.03, dtype=torch.float64, device="cuda")
+    v += torch.rand_like(v) * 1e-29
+    plan = propagator.make_plan(grid, v, m, 1e-6)
+    psi = (torch.randn(nx, ny, nz, dtype=torch.complex128, device="cuda") * 1e-3).contiguous()
+    P = _lib
+    passes = [("Z_MID", P.PASS_Z_MID, 40), ("Y_FWD", P.PASS_Y_FWD, 32), ("X_KIN", P.PASS_X_KIN, 32),
+              ("Y_INV", P.PASS_Y_INV, 32), ("Z_FIRST", P.PASS_Z_FIRST, 40), ("Z_LAST", P.PASS_Z_LAST, 40),
+              ("Z_FWD", P.PASS_Z_FWD, 32)]
+    total = 0.0
+    for name, kind, bpp in passes:
+        for _ in range(3):
+            plan.native.run_pass(kind, psi, psi)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(reps):
+            plan.native.run_pass(kind, psi, psi)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / reps
+        gbs = bpp * n / (ms * 1e-3) / 1e9
+        if name in ("Z_MID", "Y_FWD", "X_KIN", "Y_INV"):
+            total += ms
+        print(f"{name:8s} {ms:8.3f} ms  {gbs:8.1f} GB/s")
+    # full steps
+    for _ in range(2):
+        plan.native.advance(psi, 5)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    plan.native.advance(psi, reps)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    print(f"sum of 4 passes {total:.3f} ms; advance {ms:.3f} ms/step = {1000 / ms:.1f} steps/s; "
+          f"{136 * n / (ms * 1e-3) / 1e9:.1f} GB/s algorithmic (136 B/pt)")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,181 @@
+"""Parity of the CUDA path (through libctap.so) with the CPU oracle and the
+reference's golden vectors.
+
+Gates (BASELINE.json north_star): complex128 wavefunction relative L2 error
+<= 1e-10 and guide populations within 1e-9 after N steps; potential bitwise.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden, oracle_grid, product_grid
+from oracle import potential as opot
+from oracle import split_step as orc
+from paper_1309_2451_b200 import magfield, observables, propagator, qgrid
+from paper_1309_2451_b200.constants import species_mass
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-10
+POP_TOL = 1e-9
+M = species_mass("li6")
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def partition_of(d, grid):
+    return observables.GuidePartition(xb1=d["xb1"], xb2=d["xb2"], grid_ref=grid)
+
+
+@pytest.mark.parametrize("name", ["ioffe_32x16x32.npz", "ctap_scaled_32x16x32.npz"])
+def test_golden_evolution_with_trace(name):
+    d = load_golden(name)
+    grid = product_grid(d)
+    psi = qgrid.Wavefunction(d["psi0"].copy(), grid)
+    plan = propagator.make_plan(grid, d["V"], float(d["mass"]), float(d["dt"]))
+    rec = observables.PopulationRecorder(partition_of(d, grid), stride=int(d["stride"]))
+    psi, stats = propagator.evolve_real(psi, plan, int(d["steps"]), [rec])
+    assert stats.n_steps == int(d["steps"])
+    assert rel_l2(psi.amplitudes, d["psi"]) <= REL_L2
+    got = rec.trace.as_array()
+    assert got.shape == d["trace"].shape
+    assert np.array_equal(got[:, 0], d["trace"][:, 0])          # time stamps exact
+    assert np.abs(got[:, 1:4] - d["trace"][:, 1:4]).max() <= POP_TOL
+    assert np.abs(got[:, 4] - d["trace"][:, 4]).max() <= 1e-12   # norm
+    assert np.abs(got[:, 5] - d["trace"][:, 5]).max() <= 1e-12   # edge mass
+
+
+def test_golden_harmonic():
+    d = load_golden("harmonic_16x16x32.npz")
+    grid = product_grid(d)
+    psi = qgrid.Wavefunction(d["psi0"].copy(), grid)
+    plan = propagator.make_plan(grid, d["V"], float(d["mass"]), float(d["dt"]))
+    psi, _ = propagator.evolve_real(psi, plan, int(d["steps"]))
+    assert rel_l2(psi.amplitudes, d["psi"]) <= REL_L2
+
+
+def test_device_potential_bitwise_golden():
+    d = load_golden("ctap_scaled_32x16x32.npz")
+    chip = magfield.ChipSegments.from_arrays(load_golden("segments_scaled.npz"))
+    grid = product_grid(d)
+    v = magfield.potential_values(chip, grid).cpu().numpy()
+    assert np.array_equal(v, d["V"])
+
+
+def test_phase_fields_match_reference_plan():
+    d = load_golden("ctap_scaled_32x16x32.npz")
+    grid = product_grid(d)
+    plan = propagator.make_plan(grid, d["V"], float(d["mass"]), float(d["dt"]))
+    # same phase bit for bit; cos/sin may differ from glibc by an ulp
+    for name in ("exp_v_half", "exp_v_full", "exp_k"):
+        got, ref = getattr(plan, name), d[name]
+        assert np.abs(got - ref).max() <= 4.5e-16, name
+    assert np.abs(np.abs(plan.exp_v_half) - 1).max() < 1e-14
+    assert np.abs(np.abs(plan.exp_k) - 1).max() < 1e-14
+
+
+def test_observables_golden():
+    d = load_golden("observables_16x8x8.npz")
+    grid = product_grid(d)
+    psi = qgrid.Wavefunction(d["amps"].copy(), grid)
+    part = observables.GuidePartition(xb1=d["xb1"], xb2=d["xb2"], grid_ref=grid)
+    pops = observables.populations(psi, part)
+    assert np.allclose(pops, d["pops"], rtol=1e-13, atol=0)
+    for m, e in zip(d["margins"], d["edges"]):
+        assert observables.edge_density(psi, int(m)) == pytest.approx(float(e), rel=1e-13)
+    assert psi.norm() == pytest.approx(float(d["norm"]), rel=1e-13)
+    assert np.allclose(observables.density_xz(psi), d["density_xz"], rtol=1e-13, atol=0)
+
+
+def test_energies_and_ground_state_golden():
+    d = load_golden("imag_16.npz")
+    grid = product_grid(d)
+    m = float(d["mass"])
+    seed = qgrid.Wavefunction(d["seed"].copy(), grid)
+    assert propagator.kinetic_expectation(seed, m) == pytest.approx(float(d["e_seed_t"]), rel=1e-12)
+    assert propagator.potential_expectation(seed, d["V"]) == pytest.approx(float(d["e_seed_v"]), rel=1e-12)
+    gs = propagator.ground_state_imaginary(grid, d["V"], seed, tol=float(d["tol"]),
+                                           tau=float(d["tau"]), mass=m)
+    # imaginary time is contracting: tiny per-step differences (exp ulps, FFT
+    # round-off) shrink, so the converged state matches closely
+    assert rel_l2(gs.amplitudes, d["gs"]) <= 1e-8
+    assert propagator.energy_expectation(gs, d["V"], m) == pytest.approx(float(d["e_gs"]), rel=1e-10)
+    assert abs(gs.norm() - 1) < 1e-12
+
+
+def test_config1_harmonic_64cube_1000_steps():
+    """BASELINE config 1: run_bench's synthetic trap on the default 64^3 grid."""
+    og = orc.Grid((64, 64, 64), (20e-6, 4e-6, 1000e-6), (-10e-6, 4e-6 / 128, 0.0))
+    v = orc.bench_potential(og, M, 5.0)
+    c = [og.origin[i] + og.extents[i] / 2 for i in range(3)]
+    a0 = orc.gaussian_packet(og, c, [e / 16 for e in og.extents])
+    f = orc.make_factors(og, v, M, 1e-6)
+    part = observables.GuidePartition(xb1=np.full(64, -3.5e-6), xb2=np.full(64, 3.5e-6))
+    ref, rows = orc.evolve_with_trace(a0.copy(), og, f, 1000, 50, part.xb1, part.xb2)
+    grid = qgrid.SimGrid(og.n, og.extents, og.origin)
+    psi = qgrid.Wavefunction(a0.copy(), grid)
+    rec = observables.PopulationRecorder(part, stride=50)
+    psi, _ = propagator.evolve_real(psi, propagator.make_plan(grid, v, M, 1e-6), 1000, [rec])
+    assert rel_l2(psi.amplitudes, ref) <= REL_L2
+    assert np.abs(rec.trace.as_array()[:, 1:4] - rows[:, 1:4]).max() <= POP_TOL
+
+
+def test_ctap_scaled_chip_64cube_1000_steps():
+    """Phase-sensitive CTAP case (|phi_V| >= 1312 rad per step): device V bitwise
+    equal to the oracle's, then 1000 steps within 1e-10."""
+    chip_d = load_golden("segments_scaled.npz")
+    chip = magfield.ChipSegments.from_arrays(chip_d)
+    ny = 64
+    og = orc.Grid((64, ny, 64), (20e-6, 4e-6, 250e-6), (-10e-6, 4e-6 / ny / 2, 0.0))
+    grid = qgrid.SimGrid(og.n, og.extents, og.origin)
+    v_dev = magfield.potential_values(chip, grid)
+    v = opot.potential_from_chip(chip_d, og.axis(0), og.axis(1), og.axis(2))
+    assert np.array_equal(v_dev.cpu().numpy(), v)
+    phi_full = (-1.0 * (v / orc.unit_energy(M))) * (1e-6 / orc.unit_time(M))
+    assert phi_full.max() < -1300.0   # Ioffe floor: large phases every step
+    a0 = orc.gaussian_packet(og, (-3.5e-6, 2e-6, 60e-6), (0.5e-6, 0.3e-6, 10e-6))
+    f = orc.make_factors(og, v, M, 1e-6)
+    xb = np.full(64, 1.75e-6)
+    ref, rows = orc.evolve_with_trace(a0.copy(), og, f, 1000, 100, -xb, xb)
+    psi = qgrid.Wavefunction(a0.copy(), grid)
+    part = observables.GuidePartition(xb1=-xb, xb2=xb, grid_ref=grid)
+    rec = observables.PopulationRecorder(part, stride=100)
+    psi, _ = propagator.evolve_real(psi, propagator.make_plan(grid, v_dev, M, 1e-6), 1000, [rec])
+    assert rel_l2(psi.amplitudes, ref) <= REL_L2
+    assert np.abs(rec.trace.as_array()[:, 1:4] - rows[:, 1:4]).max() <= POP_TOL
+
+
+@pytest.mark.parametrize("n", [(8, 8, 8), (16, 32, 8), (128, 8, 16), (8, 256, 32), (1024, 8, 8),
+                               (8, 1024, 8), (8, 8, 1024), (32, 512, 16)])
+def test_fft_every_axis_length(n):
+    """Axis lengths 8..1024 on every axis against numpy's FFT."""
+    rng = np.random.default_rng(sum(n))
+    a = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    grid = qgrid.SimGrid(n, (1e-5,) * 3, (0.0,) * 3)
+    plan = propagator._aux_plan(grid)
+    d = torch.from_numpy(a.copy()).cuda()
+    plan.fft3d(d, -1)
+    ref = np.fft.fftn(a)
+    assert rel_l2(d.cpu().numpy(), ref) <= 1e-14
+    plan.fft3d(d, +1)
+    assert rel_l2(d.cpu().numpy() / a.size, a) <= 1e-14
+
+
+def test_determinism_bitwise():
+    d = load_golden("ioffe_32x16x32.npz")
+    grid = product_grid(d)
+
+    def run():
+        psi = qgrid.Wavefunction(d["psi0"].copy(), grid)
+        plan = propagator.make_plan(grid, d["V"], M, 1e-6)
+        rec = observables.PopulationRecorder(partition_of(d, grid), stride=10)
+        psi, _ = propagator.evolve_real(psi, plan, 50, [rec])
+        return psi.amplitudes, rec.trace.as_array()
+
+    a1, t1 = run()
+    a2, t2 = run()
+    assert np.array_equal(a1, a2)
+    assert np.array_equal(t1, t2)
