@@ -79,7 +79,10 @@ typedef struct ctap_plan_desc {
   int32_t mode;     /* ctap_mode */
   int32_t slab_p;   /* number of x-slab ranks (1 = single GPU) */
   int32_t slab_r;   /* this rank */
-  int32_t reserved;
+  int32_t phase_tables; /* 1: keep exp(-i V dt) and exp(-i k^2 dt/2) as complex
+                           tables in HBM (no sincos per step, +24 B/pt/step);
+                           0: recompute them per point every step.  Both use
+                           the identical phase arithmetic (real time only). */
 } ctap_plan_desc;
 
 /* make_plan (propagator.py:55-81).  kx2/ky2/kz2 are HOST arrays of the squared

@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libctap.so")
+# CTAP_LIBRARY overrides the in-tree build (used for A/B kernel experiments)
+LIB_PATH = os.environ.get("CTAP_LIBRARY") or os.path.join(_HERE, "lib", "libctap.so")
 
 CTAP_OK = 0
 CTAP_EINVAL = 1
@@ -44,7 +45,7 @@ class CtapPlanDesc(ctypes.Structure):
         ("mode", ctypes.c_int32),
         ("slab_p", ctypes.c_int32),
         ("slab_r", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("phase_tables", ctypes.c_int32),
     ]
 
 

@@ -14,7 +14,6 @@ cudaError_t ctap_run_observe(const ctap_plan* p, const void* psi, const double* 
 cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, cudaStream_t st);
 cudaError_t ctap_run_v_sums(const ctap_plan* p, const void* psi, double* out, cudaStream_t st);
 cudaError_t ctap_run_density_xz(const ctap_plan* p, const void* psi, double* out, cudaStream_t st);
-cudaError_t ctap_run_phase_field(const ctap_plan* p, int which, void* out, cudaStream_t st);
 cudaError_t ctap_run_scale(const ctap_plan* p, void* psi, double d, cudaStream_t st);
 cudaError_t ctap_run_potential(const double* xs, int64_t nx, const double* ys, int64_t ny, const double* zs,
                                int64_t nz, const double* seg_a, const double* seg_b, const double* seg_cur,
@@ -98,7 +97,8 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   p->v_dev = v_dev;
   p->inv_scale = 1.0 / (double)(d->n[0] * d->n[1] * d->n[2]);  // exact: power of two
   const double* k2h[3] = {kx2, ky2, kz2};
-  cudaError_t e = cudaSuccess;
+  // plan creation is rare: order it against whatever stream produced V
+  cudaError_t e = cudaDeviceSynchronize();
   for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
     e = cudaMalloc((void**)&p->k2_dev[i], sizeof(double) * d->n[i]);
     if (e == cudaSuccess) e = cudaMemcpy(p->k2_dev[i], k2h[i], sizeof(double) * d->n[i], cudaMemcpyHostToDevice);
@@ -111,6 +111,16 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   p->red_blocks = sms * 4;
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->red_partial, sizeof(double) * 8 * p->red_blocks);
+  const size_t nloc = (size_t)p->nx_local * d->n[1] * d->n[2];
+  if (e == cudaSuccess) e = cudaMalloc((void**)&p->vi_dev, sizeof(double) * nloc);
+  if (e == cudaSuccess) e = ctap_run_v_internal(p, 0);
+  if (e == cudaSuccess && d->phase_tables && d->mode == CTAP_REAL_TIME) {
+    e = cudaMalloc((void**)&p->expv_dev, sizeof(double2) * nloc);
+    if (e == cudaSuccess) e = ctap_run_phase_field(p, 1, p->expv_dev, 0);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&p->expk_dev, sizeof(double2) * nloc);
+    if (e == cudaSuccess) e = ctap_run_phase_field(p, 3, p->expk_dev, 0);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     ctap_plan_destroy(p);
     return cuda_fail(e, "ctap_plan_create");
@@ -124,6 +134,9 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
   for (int i = 0; i < 3; ++i) cudaFree(p->k2_dev[i]);
   cudaFree(p->twiddles);
   cudaFree(p->red_partial);
+  cudaFree(p->vi_dev);
+  cudaFree(p->expv_dev);
+  cudaFree(p->expk_dev);
   delete p;
   return CTAP_OK;
 }

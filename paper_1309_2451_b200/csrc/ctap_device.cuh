@@ -12,6 +12,9 @@
 // a pointwise multiply can be applied in registers and an inverse transform
 // can start right away without another exchange (this is what lets one
 // kernel apply  F^-1 . diag(phase) . F  along an axis in a single HBM sweep).
+//
+// Index arithmetic is 32-bit throughout: a local slab never exceeds 2^30
+// points (axes are <= 1024).
 #pragma once
 
 #include <cstdint>
@@ -127,6 +130,20 @@ struct SmemStrided {  // column-fastest tile: element i of column c at i*8 + c
   __device__ __forceinline__ double2& at(int i) const { return base[i * 8]; }
 };
 
+// Barrier among the threads that share one exchange buffer.
+struct SyncBlock {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct SyncWarp {  // the whole line lives inside one warp
+  __device__ __forceinline__ void operator()() const { __syncwarp(); }
+};
+struct SyncNamed {  // T threads (a multiple of 32) of one line: named barrier
+  int id, count;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  }
+};
+
 // One Stockham stage on the eight registers of thread t.
 //   radix R, stride Ns (product of earlier radices), line length L.
 // Input: v[m] = x[t + m*T].  Output scattered to smem (unless last stage, in
@@ -163,9 +180,9 @@ __device__ __forceinline__ void stockham_stage(double2* v, int t, const double2*
   }
 }
 
-template <int L, int S, int DIR, typename Smem>
+template <int L, int S, int DIR, typename Smem, typename Sync>
 __device__ __forceinline__ void fft_stages(double2* v, int t, const double2* __restrict__ tw, Smem sm,
-                                           void (*sync)()) {
+                                           Sync sync) {
   using P = Plan<L>;
   constexpr int T = P::T;
   if constexpr (S < P::nstages) {
@@ -183,32 +200,153 @@ __device__ __forceinline__ void fft_stages(double2* v, int t, const double2* __r
   }
 }
 
-__device__ __forceinline__ void block_sync() { __syncthreads(); }
-
 // Full in-register/shared 1D FFT of the thread's line.  On entry v[m] holds
-// x[t + m*T], on exit X[t + m*T] (unnormalized, sign DIR).
-template <int L, int DIR, typename Smem>
-__device__ __forceinline__ void line_fft(double2* v, int t, const double2* __restrict__ tw, Smem sm) {
-  fft_stages<L, 0, DIR>(v, t, tw, sm, block_sync);
+// x[t + m*T], on exit X[t + m*T] (unnormalized, sign DIR).  Every thread that
+// shares the exchange buffer must call it (barriers inside).
+template <int L, int DIR, typename Smem, typename Sync>
+__device__ __forceinline__ void line_fft(double2* v, int t, const double2* __restrict__ tw, Smem sm, Sync sync) {
+  fft_stages<L, 0, DIR>(v, t, tw, sm, sync);
 }
 
 // --- exact phase recipes (reference propagator.py:61-68, qgrid.py:98-117) ---
 // These products must not be contracted into FMAs: a systematic one-ulp phase
 // error fails the 1e-10 parity gate.
 
-// potential phase: (coef * (V - shift)/E0) * dt_i with coef -0.5 (half) or -1.0 (full)
-__device__ __forceinline__ double v_phase(double v, double shift, double e0, double coef, double dt_i) {
-  double vi = __ddiv_rn(__dsub_rn(v, shift), e0);
+// v_i = (V - shift) / E0  (evaluated once per plan, propagator.py:65 / :75)
+__device__ __forceinline__ double v_internal(double v, double shift, double e0) {
+  return __ddiv_rn(__dsub_rn(v, shift), e0);
+}
+// potential phase (coef * v_i) * dt_i, coef -0.5 (half step) or -1.0 (full step)
+__device__ __forceinline__ double v_phase_i(double vi, double coef, double dt_i) {
   return __dmul_rn(__dmul_rn(coef, vi), dt_i);
 }
-__device__ __forceinline__ double v_phase_real(double v, double e0, double coef, double dt_i) {
-  double vi = __ddiv_rn(v, e0);
-  return __dmul_rn(__dmul_rn(coef, vi), dt_i);
+__device__ __forceinline__ double v_phase(double v, double shift, double e0, double coef, double dt_i) {
+  return v_phase_i(v_internal(v, shift, e0), coef, dt_i);
 }
 // kinetic phase: (-0.5 * (((kx2 + ky2) + kz2) * L0^2)) * dt_i
 __device__ __forceinline__ double k_phase(double kx2, double ky2, double kz2, double len2, double dt_i) {
   double k2 = __dadd_rn(__dadd_rn(kx2, ky2), kz2);
   return __dmul_rn(__dmul_rn(-0.5, __dmul_rn(k2, len2)), dt_i);
+}
+
+// cos/sin(k pi/32), k = 0..63, correctly rounded (50-digit decimal series)
+__device__ const double2 kSinCosTab[64] = {
+    {1.0, 0.0},
+    {0.9951847266721969, 0.0980171403295606},
+    {0.9807852804032304, 0.19509032201612828},
+    {0.9569403357322088, 0.2902846772544624},
+    {0.9238795325112867, 0.3826834323650898},
+    {0.881921264348355, 0.47139673682599764},
+    {0.8314696123025452, 0.5555702330196022},
+    {0.773010453362737, 0.6343932841636455},
+    {0.7071067811865476, 0.7071067811865476},
+    {0.6343932841636455, 0.773010453362737},
+    {0.5555702330196022, 0.8314696123025452},
+    {0.47139673682599764, 0.881921264348355},
+    {0.3826834323650898, 0.9238795325112867},
+    {0.2902846772544624, 0.9569403357322088},
+    {0.19509032201612828, 0.9807852804032304},
+    {0.0980171403295606, 0.9951847266721969},
+    {2.1014944983910808e-55, 1.0},
+    {-0.0980171403295606, 0.9951847266721969},
+    {-0.19509032201612828, 0.9807852804032304},
+    {-0.2902846772544624, 0.9569403357322088},
+    {-0.3826834323650898, 0.9238795325112867},
+    {-0.47139673682599764, 0.881921264348355},
+    {-0.5555702330196022, 0.8314696123025452},
+    {-0.6343932841636455, 0.773010453362737},
+    {-0.7071067811865476, 0.7071067811865476},
+    {-0.773010453362737, 0.6343932841636455},
+    {-0.8314696123025452, 0.5555702330196022},
+    {-0.881921264348355, 0.47139673682599764},
+    {-0.9238795325112867, 0.3826834323650898},
+    {-0.9569403357322088, 0.2902846772544624},
+    {-0.9807852804032304, 0.19509032201612828},
+    {-0.9951847266721969, 0.0980171403295606},
+    {-1.0, -4.164292633035009e-54},
+    {-0.9951847266721969, -0.0980171403295606},
+    {-0.9807852804032304, -0.19509032201612828},
+    {-0.9569403357322088, -0.2902846772544624},
+    {-0.9238795325112867, -0.3826834323650898},
+    {-0.881921264348355, -0.47139673682599764},
+    {-0.8314696123025452, -0.5555702330196022},
+    {-0.773010453362737, -0.6343932841636455},
+    {-0.7071067811865476, -0.7071067811865476},
+    {-0.6343932841636455, -0.773010453362737},
+    {-0.5555702330196022, -0.8314696123025452},
+    {-0.47139673682599764, -0.881921264348355},
+    {-0.3826834323650898, -0.9238795325112867},
+    {-0.2902846772544624, -0.9569403357322088},
+    {-0.19509032201612828, -0.9807852804032304},
+    {-0.0980171403295606, -0.9951847266721969},
+    {1.1132433694450584e-53, -1.0},
+    {0.0980171403295606, -0.9951847266721969},
+    {0.19509032201612828, -0.9807852804032304},
+    {0.2902846772544624, -0.9569403357322088},
+    {0.3826834323650898, -0.9238795325112867},
+    {0.47139673682599764, -0.881921264348355},
+    {0.5555702330196022, -0.8314696123025452},
+    {0.6343932841636455, -0.773010453362737},
+    {0.7071067811865476, -0.7071067811865476},
+    {0.773010453362737, -0.6343932841636455},
+    {0.8314696123025452, -0.5555702330196022},
+    {0.881921264348355, -0.47139673682599764},
+    {0.9238795325112867, -0.3826834323650898},
+    {0.9569403357322088, -0.2902846772544624},
+    {0.9807852804032304, -0.19509032201612828},
+    {0.9951847266721969, -0.0980171403295606}
+};
+
+// polynomial/reduction constants as constant-bank operands (no per-use
+// register materialisation)
+__constant__ double kSC[12] = {
+    10.185916357881302,        // 0: 32/pi
+    0x1.921fb54000000p-4,      // 1: pi/32 = C1 + C2 + C3 (27 + 27 + 53 bits)
+    0x1.10b4610000000p-34,     // 2
+    0x1.a62633145c06ep-62,     // 3
+    2.7557319223985893e-06,    // 4: 1/9!
+    -1.9841269841269841e-04,   // 5: -1/7!
+    8.3333333333333333e-03,    // 6: 1/5!
+    -1.6666666666666666e-01,   // 7: -1/3!
+    2.4801587301587302e-05,    // 8: 1/8!
+    -1.3888888888888889e-03,   // 9: -1/6!
+    4.1666666666666664e-02,    // 10: 1/4!
+    6755399441055744.0,        // 11: 1.5 * 2^52
+};
+
+// sincos for the phase factors.  The phase itself is exact (computed with the
+// recipes above); only cos/sin of it are evaluated here, to ~1.5 ulp:
+//   n = rint(phi * 32/pi) via the 1.5*2^52 magic constant, r = phi - n*pi/32
+//   by a three-term Cody-Waite split (exact first term for |n| < 2^26),
+//   Taylor polynomials on |r| <= pi/64 (sin to r^9, cos to r^8), and a
+//   rotation by the tabulated (cos, sin)(n pi/32).
+// About 19 FP64 operations against ~40 FP64 + ~70 other instructions for the
+// library sincos; |phi| >= 2^22 falls back to the library (never on CTAP
+// grids, where |phi| < 1e6).  Errors of an ulp in the factor are harmless
+// (only the phase must be bit-exact).
+__device__ __forceinline__ void fast_sincos(double phi, double* s, double* c) {
+  if (fabs(phi) < 4194304.0) {
+    const double t = fma(phi, kSC[0], kSC[11]);
+    const int n = __double2loint(t);
+    const double nf = t - kSC[11];
+    double r = fma(-nf, kSC[1], phi);
+    r = fma(-nf, kSC[2], r);
+    r = fma(-nf, kSC[3], r);
+    const double r2 = r * r;
+    double ps = fma(r2, kSC[4], kSC[5]);
+    ps = fma(r2, ps, kSC[6]);
+    ps = fma(r2, ps, kSC[7]);
+    const double sr = fma(r * r2, ps, r);
+    double pc = fma(r2, kSC[8], kSC[9]);
+    pc = fma(r2, pc, kSC[10]);
+    pc = fma(r2, pc, -0.5);
+    const double cr = fma(r2, pc, 1.0);
+    const double2 tb = __ldg(&kSinCosTab[n & 63]);
+    *c = fma(tb.x, cr, -(tb.y * sr));
+    *s = fma(tb.y, cr, tb.x * sr);
+  } else {
+    sincos(phi, s, c);
+  }
 }
 
 }  // namespace ctap

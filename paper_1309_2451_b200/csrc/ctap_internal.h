@@ -37,11 +37,16 @@ struct ctap_plan {
   int mode;  // 0 real, 1 imaginary
   double e0, dt_i, len2, v_shift;
   double inv_scale;        // 1 / (nx ny nz), exact power of two
-  const double* v_dev;     // caller-owned potential slab
+  const double* v_dev;     // caller-owned potential slab (J)
+  double* vi_dev;          // v_i = (V - v_shift) / e0, plan-owned (propagator.py:65, :75)
+  double2* expv_dev;       // optional table exp(-i v_i dt_i)       (phase_tables, real time)
+  double2* expk_dev;       // optional table exp(-i k^2 dt/2) / N, x-pass layout
   double* k2_dev[3];       // squared wavenumbers per axis (global lengths)
   double2* twiddles;       // concatenated exp(-2 pi i m / L), L = 8..1024
   double* red_partial;     // reduction scratch
   int red_blocks;
 };
 
+cudaError_t ctap_run_v_internal(const ctap_plan* p, cudaStream_t st);
+cudaError_t ctap_run_phase_field(const ctap_plan* p, int which, void* out, cudaStream_t st);
 cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* out, cudaStream_t st);

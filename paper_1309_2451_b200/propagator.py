@@ -17,6 +17,7 @@ four fused axis passes per step.
 from __future__ import annotations
 
 import ctypes
+import os
 import sys
 import time as _time
 import weakref
@@ -31,6 +32,10 @@ from .qgrid import UnitSystem, Wavefunction, as_simgrid, grid_key, same_grid, wr
 REAL_TIME = "real_time"
 IMAGINARY_TIME = "imaginary_time"
 
+# default phase mode of make_plan; the
+# environment variable is for A/B measurements
+DEFAULT_PHASE_TABLES = os.environ.get("CTAP_PHASE_TABLES", "0") == "1"
+
 
 class ConvergenceError(RuntimeError):
     """Imaginary-time relaxation failed to reach the tolerance."""
@@ -44,7 +49,8 @@ class NativePlan:
     """Owns one ctap_plan (include/ctap.h) and the device buffers it points at."""
 
     def __init__(self, grid, v_dev: torch.Tensor | None, mass: float, dt: float,
-                 mode: str = REAL_TIME, v_shift: float = 0.0, slab_p: int = 1, slab_r: int = 0):
+                 mode: str = REAL_TIME, v_shift: float = 0.0, slab_p: int = 1, slab_r: int = 0,
+                 phase_tables: bool = False):
         lib = _lib.load()
         dev = _device.require_cuda()
         self.grid = as_simgrid(grid)
@@ -59,6 +65,7 @@ class NativePlan:
         desc.mode = _lib.REAL_TIME_MODE if mode == REAL_TIME else _lib.IMAGINARY_TIME_MODE
         desc.slab_p = int(slab_p)
         desc.slab_r = int(slab_r)
+        desc.phase_tables = int(bool(phase_tables))
         self.desc = desc
         # squared wavenumbers exactly as k_squared() forms them (qgrid.py:112-115)
         self._k2 = [np.ascontiguousarray(self.grid.k_axis(i) ** 2) for i in range(3)]
@@ -172,8 +179,13 @@ class StepPlan:
 
 
 def make_plan(grid, potential, mass: float, dt: float, mode: str = REAL_TIME,
-              threads: int = 1) -> StepPlan:
-    """make_plan (propagator.py:55-81)."""
+              threads: int = 1, *, phase_tables: bool | None = None) -> StepPlan:
+    """make_plan (propagator.py:55-81).
+
+    `threads` is accepted for signature compatibility (the device decides its
+    own parallelism).  `phase_tables` (B200 extension) keeps exp(-i V dt) and
+    exp(-i k^2 dt/2) as HBM tables instead of recomputing them per step; the
+    phases are bit-identical either way.  None picks the faster mode."""
     if mode not in (REAL_TIME, IMAGINARY_TIME):
         raise ValueError(f"unknown mode {mode!r}")
     if tuple(potential.shape) != tuple(grid.n):
@@ -187,7 +199,9 @@ def make_plan(grid, potential, mass: float, dt: float, mode: str = REAL_TIME,
         shift = 0.0
     else:
         shift = float(v_dev.min().item())
-    native = NativePlan(grid, v_dev, mass, dt, mode, v_shift=shift)
+    if phase_tables is None:
+        phase_tables = DEFAULT_PHASE_TABLES
+    native = NativePlan(grid, v_dev, mass, dt, mode, v_shift=shift, phase_tables=phase_tables)
     return StepPlan(grid=grid, dt=dt, mode=mode, mass=mass, potential=potential,
                     threads=threads, native=native)
 

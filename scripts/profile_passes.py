@@ -1,0 +1,25 @@
+"""Launch each split-step pass kind twice (warm-up + profiled) for ncu.
+
+usage: python scripts/profile_passes.py NX NY NZ
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+from paper_1309_2451_b200 import _lib, propagator, qgrid
+from paper_1309_2451_b200.constants import muB, species_mass
+
+nx, ny, nz = (int(v) for v in sys.argv[1:4])
+grid = qgrid.make_grid(nx, ny, nz, (20e-6, 4e-6, 1000e-6), origin=(-10e-6, 4e-6 / ny / 2, 0.0))
+v = torch.full((nx, ny, nz), muB / 2 * 0.03, dtype=torch.float64, device="cuda")
+plan = propagator.make_plan(grid, v, species_mass("li6"), 1e-6)
+psi = torch.randn(nx, ny, nz, dtype=torch.complex128, device="cuda")
+kinds = [getattr(_lib, 'PASS_' + k) for k in (sys.argv[4].split(',') if len(sys.argv) > 4 else ['Z_MID', 'Y_FWD', 'X_KIN', 'Z_FWD', 'Z_FIRST'])]
+for kind in kinds:
+    for _ in range(2):
+        plan.native.run_pass(kind, psi, psi)
+torch.cuda.synchronize()
+print("ok")
