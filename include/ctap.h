@@ -79,16 +79,19 @@ typedef struct ctap_plan_desc {
   int32_t mode;     /* ctap_mode */
   int32_t slab_p;   /* number of x-slab ranks (1 = single GPU) */
   int32_t slab_r;   /* this rank */
-  int32_t phase_tables; /* 1: keep exp(-i V dt) and exp(-i k^2 dt/2) as complex
-                           tables in HBM (no sincos per step, +24 B/pt/step);
-                           0: recompute them per point every step.  Both use
-                           the identical phase arithmetic (real time only). */
+  int32_t phase_tables; /* bit 0: keep exp(-i V dt) as a complex table in HBM
+                           (+8 B/pt/step, no sincos in the z pass); bit 1: keep
+                           exp(-i k^2 dt/2)/N as a table (+16 B/pt/step).  A
+                           clear bit recomputes that factor per point every
+                           step.  All variants use the identical phase
+                           arithmetic (real time only; ignored otherwise). */
 } ctap_plan_desc;
 
 /* make_plan (propagator.py:55-81).  kx2/ky2/kz2 are HOST arrays of the squared
  * angular wavenumbers k_axis(i)**2 in m^-2 (qgrid.py:98-117), full global
  * length.  v_dev is the caller's device potential slab (nx/slab_p, ny, nz),
- * which must stay alive for the plan's lifetime.  The phase factors are never
+ * which must stay alive for the plan's lifetime; NULL makes a plan that only
+ * serves FFTs and reductions (the potential passes then fail with EINVAL).  The phase factors are never
  * materialised: they are recomputed per point with the reference's exact
  * operation order inside the passes. */
 CTAP_API int ctap_plan_create(const ctap_plan_desc* desc, const double* kx2, const double* ky2,

@@ -81,7 +81,6 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   int P = d->slab_p < 1 ? 1 : d->slab_p;
   if (d->n[0] % P || d->n[1] % P) return fail(CTAP_EINVAL, "nx and ny must be divisible by the %d slab ranks", P);
   if (d->slab_r < 0 || d->slab_r >= P) return fail(CTAP_EINVAL, "slab rank %d out of range", d->slab_r);
-  if (!v_dev) return fail(CTAP_EINVAL, "potential pointer is null");
 
   ctap_plan* p = new ctap_plan();
   std::memset(p, 0, sizeof *p);
@@ -112,12 +111,16 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   p->red_blocks = sms * 4;
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->red_partial, sizeof(double) * 8 * p->red_blocks);
   const size_t nloc = (size_t)p->nx_local * d->n[1] * d->n[2];
-  if (e == cudaSuccess) e = cudaMalloc((void**)&p->vi_dev, sizeof(double) * nloc);
-  if (e == cudaSuccess) e = ctap_run_v_internal(p, 0);
-  if (e == cudaSuccess && d->phase_tables && d->mode == CTAP_REAL_TIME) {
+  if (v_dev) {  // a plan without a potential only serves FFTs and reductions
+    if (e == cudaSuccess) e = cudaMalloc((void**)&p->vi_dev, sizeof(double) * nloc);
+    if (e == cudaSuccess) e = ctap_run_v_internal(p, 0);
+  }
+  if (e == cudaSuccess && v_dev && (d->phase_tables & 1) && d->mode == CTAP_REAL_TIME) {
     e = cudaMalloc((void**)&p->expv_dev, sizeof(double2) * nloc);
     if (e == cudaSuccess) e = ctap_run_phase_field(p, 1, p->expv_dev, 0);
-    if (e == cudaSuccess) e = cudaMalloc((void**)&p->expk_dev, sizeof(double2) * nloc);
+  }
+  if (e == cudaSuccess && (d->phase_tables & 2) && d->mode == CTAP_REAL_TIME) {
+    e = cudaMalloc((void**)&p->expk_dev, sizeof(double2) * nloc);
     if (e == cudaSuccess) e = ctap_run_phase_field(p, 3, p->expk_dev, 0);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -145,6 +148,8 @@ CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, vo
   if (!p || !in || !out) return fail(CTAP_EINVAL, "null argument");
   if (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_X_INV) return fail(CTAP_EINVAL, "unknown pass %d", kind);
   if (kind <= CTAP_PASS_Z_LAST && in != out) return fail(CTAP_EINVAL, "z passes run in place");
+  if ((kind == CTAP_PASS_Z_FIRST || kind == CTAP_PASS_Z_MID || kind == CTAP_PASS_Z_LAST) && !p->vi_dev)
+    return fail(CTAP_EINVAL, "plan has no potential");
   CUDA_TRY(ctap_run_pass(p, kind, in, out, (cudaStream_t)stream), "ctap_pass");
   return CTAP_OK;
 }
@@ -153,6 +158,7 @@ CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
   if (!p || !psi) return fail(CTAP_EINVAL, "null argument");
   if (n < 0) return fail(CTAP_EINVAL, "n_steps must be >= 0");
   if (p->slab_p != 1) return fail(CTAP_EINVAL, "ctap_advance drives single-GPU plans; use ctap_pass for slabs");
+  if (!p->vi_dev) return fail(CTAP_EINVAL, "plan has no potential");
   if (n == 0) return CTAP_OK;
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Z_FIRST, psi, psi, st), "ctap_advance");
@@ -204,6 +210,7 @@ CTAP_API int ctap_k2_sums(ctap_plan* p, const void* phi, double* out, void* stre
 
 CTAP_API int ctap_v_sums(ctap_plan* p, const void* psi, double* out, void* stream) {
   if (!p || !psi || !out) return fail(CTAP_EINVAL, "null argument");
+  if (!p->v_dev) return fail(CTAP_EINVAL, "plan has no potential");
   CUDA_TRY(ctap_run_v_sums(p, psi, out, (cudaStream_t)stream), "ctap_v_sums");
   return CTAP_OK;
 }
@@ -211,6 +218,7 @@ CTAP_API int ctap_v_sums(ctap_plan* p, const void* psi, double* out, void* strea
 CTAP_API int ctap_phase_field(ctap_plan* p, int32_t which, void* out, void* stream) {
   if (!p || !out) return fail(CTAP_EINVAL, "null argument");
   if (which < 0 || which > 2) return fail(CTAP_EINVAL, "which must be 0 (v_half), 1 (v_full) or 2 (k)");
+  if (which < 2 && !p->vi_dev) return fail(CTAP_EINVAL, "plan has no potential");
   CUDA_TRY(ctap_run_phase_field(p, which, out, (cudaStream_t)stream), "ctap_phase_field");
   return CTAP_OK;
 }

@@ -9,15 +9,15 @@
 // sweeps:   [z^-1 . V . z]   y   [x . K . x^-1]   y^-1
 // (segment ends use [Vh . z] and [z^-1 . Vh] instead of the middle z pass).
 //
-// All passes share one tile kernel.  A tile is 8 lines x L points; thread
-// (t, col) owns points t + m*T (m < 8) of line col, so the 8 lanes of a
-// quarter-warp hold the same point of 8 lines:
-//   y/x passes: the 8 lines are 8 consecutive z columns -> every warp access
-//               is 4 rows x 128 contiguous bytes;
-//   z passes:   the 8 lines are 8 consecutive z-lines (stride L) -> 8 rows x
-//               64 contiguous bytes.
-// Either way twiddle gathers see at most 4 distinct addresses per warp and the
-// exchange buffer [i][8] is bank-conflict free.
+// Two kernel shapes:
+//   zline_kernel  z passes.  Lines are contiguous; T = L/8 consecutive lanes
+//                 own one line (every warp access is 512 contiguous bytes),
+//                 the exchange buffer is a padded line, and only the threads
+//                 of one line synchronise (warp or named barrier).
+//   tile_kernel   y and x passes.  A tile is 8 consecutive z columns x the
+//                 whole line: thread (t, col) owns points t + m*T of column
+//                 col, so every warp access is 4 rows x 128 contiguous bytes
+//                 and the [i][8] exchange buffer is bank-conflict free.
 //
 // Phase factors come either from the per-point exact recipes (on the fly,
 // 8 B/pt of v_i = V/E0 per step) or from plan-owned complex tables of the
@@ -26,12 +26,144 @@
 #include "ctap_device.cuh"
 #include "ctap_internal.h"
 
-// resident threads per SM the register allocation is sized for
+// resident threads per SM the register allocation of the strided kernels is
+// sized for, and min blocks per SM of the z kernels (256 threads)
 #ifndef CTAP_OCC
 #define CTAP_OCC 1024
 #endif
+#ifndef CTAP_Z_MINB
+#define CTAP_Z_MINB 4
+#endif
+#ifndef CTAP_Z_MINB_TAB
+#define CTAP_Z_MINB_TAB 2
+#endif
+#ifndef CTAP_OCC_TAB
+#define CTAP_OCC_TAB 512
+#endif
 
 namespace ctap {
+
+enum TileKind { T_FWD, T_INV, T_KIN, T_VFIRST, T_VMID, T_VLAST };
+
+struct PhaseArgs {
+  const double* vi;     // v_i = (V - shift)/E0 at the element offsets of psi (z passes)
+  const double2* expv;  // exp(-i v_i dt_i) table (z passes, VTAB)
+  const double* kx2;    // k^2 along the pass axis (x pass)
+  const double* ky2;    // k^2 along the outer axis, global
+  const double* kz2;    // k^2 along z
+  const double2* expk;  // exp(-i k^2 dt/2)/N table in the x-pass layout (KTAB)
+  uint32_t outer_off;   // global index of outer o = 0
+  double len2, dt_i;
+  double scale;         // folded inverse normalisation 1/N (power of two)
+  int imag;             // imaginary time: real decay factors
+};
+
+// v *= exp(i coef v_i dt) (real time) or exp(coef v_i dt) (imaginary time)
+__device__ __forceinline__ void mul_vphase(double2& v, double vi, double coef, const PhaseArgs& a) {
+  const double phi = v_phase_i(vi, coef, a.dt_i);
+  if (a.imag) {
+    const double f = exp(phi);
+    v = make_double2(v.x * f, v.y * f);
+  } else {
+    double s, c;
+    fast_sincos(phi, &s, &c);
+    v = cmul(v, make_double2(c, s));
+  }
+}
+
+// v *= exp(-i k^2 dt/2) / N at (kx2, ky2, kz2)
+__device__ __forceinline__ void mul_kphase(double2& v, double kx2, double ky2, double kz2, const PhaseArgs& a) {
+  const double phi = k_phase(kx2, ky2, kz2, a.len2, a.dt_i);
+  if (a.imag) {
+    const double f = exp(phi) * a.scale;
+    v = make_double2(v.x * f, v.y * f);
+  } else {
+    double s, c;
+    fast_sincos(phi, &s, &c);
+    v = cmul(v, make_double2(c * a.scale, s * a.scale));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// z passes
+// ---------------------------------------------------------------------------
+
+template <int L>
+struct ZCfg {
+  static constexpr int T = L / kElems;
+  static constexpr int C = (256 / T) > 0 ? (256 / T) : 1;  // lines per block
+  static constexpr int threads = C * T;
+  static constexpr int smem_line = L + L / 8;             // padded double2 per line
+  static constexpr size_t smem = (size_t)C * smem_line * sizeof(double2);
+};
+
+struct ZArgs {
+  double2* psi;
+  uint32_t nlines;  // nx_local * ny
+  PhaseArgs ph;
+};
+
+template <int L, int KIND, bool VTAB, typename Sync>
+__device__ __forceinline__ void z_body(const ZArgs& a, double2* v, int t, uint32_t off, bool active,
+                                       const double2* __restrict__ tw, SmemContig sm, Sync sync) {
+  constexpr int T = L / kElems;
+  if constexpr (KIND == T_FWD) {
+    line_fft<L, -1>(v, t, tw, sm, sync);
+  } else if constexpr (KIND == T_INV) {
+    line_fft<L, +1>(v, t, tw, sm, sync);
+  } else if constexpr (KIND == T_VFIRST) {  // Vh, then forward
+    if (active) {
+#pragma unroll
+      for (int m = 0; m < kElems; ++m) mul_vphase(v[m], __ldcg(&a.ph.vi[off + t + m * T]), -0.5, a.ph);
+    }
+    line_fft<L, -1>(v, t, tw, sm, sync);
+  } else {  // T_VMID: inverse, V, forward; T_VLAST: inverse, Vh
+    line_fft<L, +1>(v, t, tw, sm, sync);
+    if (active) {
+#pragma unroll
+      for (int m = 0; m < kElems; ++m) {
+        if (KIND == T_VMID && VTAB) v[m] = cmul(v[m], __ldcg(&a.ph.expv[off + t + m * T]));
+        else mul_vphase(v[m], __ldcg(&a.ph.vi[off + t + m * T]), KIND == T_VMID ? -1.0 : -0.5, a.ph);
+      }
+    }
+    if constexpr (KIND == T_VMID) line_fft<L, -1>(v, t, tw, sm, sync);
+  }
+}
+
+// register budget per kernel flavour (measured, 512^3): the table-driven
+// [z^-1 V z] wants 128 registers, the sincos flavours 64
+template <int KIND, bool VTAB>
+struct ZMinBlocks {
+  static constexpr int value = (KIND == T_VMID && VTAB) ? CTAP_Z_MINB_TAB : CTAP_Z_MINB;
+};
+
+template <int L, int KIND, bool VTAB>
+__global__ void __launch_bounds__(ZCfg<L>::threads, ZMinBlocks<KIND, VTAB>::value) zline_kernel(ZArgs a, const double2* __restrict__ tw) {
+  using C = ZCfg<L>;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x % C::T;
+  const int c = threadIdx.x / C::T;
+  const uint32_t line = blockIdx.x * C::C + c;
+  const bool active = line < a.nlines;
+  const uint32_t off = line * L;
+  SmemContig sm{smem + c * C::smem_line};
+  double2 v[kElems];
+#pragma unroll
+  for (int m = 0; m < kElems; ++m) v[m] = active ? __ldcg(&a.psi[off + t + m * C::T]) : make_double2(0.0, 0.0);
+  if constexpr (C::T <= 32) {
+    z_body<L, KIND, VTAB>(a, v, t, off, active, tw, sm, SyncWarp{});
+  } else {
+    z_body<L, KIND, VTAB>(a, v, t, off, active, tw, sm, SyncNamed{1 + c, C::T});
+  }
+  if (active) {
+#pragma unroll
+    for (int m = 0; m < kElems; ++m) __stcg(&a.psi[off + t + m * C::T], v[m]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// y and x passes
+// ---------------------------------------------------------------------------
 
 template <int L>
 struct TileCfg {
@@ -39,18 +171,14 @@ struct TileCfg {
   static constexpr int per_tile = T * 8;
   static constexpr int G = per_tile >= 128 ? 1 : 128 / per_tile;  // tiles per block
   static constexpr int threads = G * per_tile;
-  static constexpr int line_stride = L + L / 8;  // padded line of the contiguous (z) layout
-  static constexpr size_t smem = (size_t)G * 8 * line_stride * sizeof(double2);
+  static constexpr size_t smem = (size_t)G * L * 8 * sizeof(double2);
   static constexpr int minb = CTAP_OCC / threads > 0 ? CTAP_OCC / threads : 1;
-  // lanes of one warp along the line in the contiguous mapping
-  static constexpr int TL = T < 8 ? T : 8;
+  static constexpr int minb_tab = CTAP_OCC_TAB / threads > 0 ? CTAP_OCC_TAB / threads : 1;
 };
 
-// Element (o, i, col) of tile (o, chunk) lives at
-//   lay(o, i) + chunk*8*cs + col*cs
-//   natural:  lay = o*so + i*si
-//   peer:     lay = o*so + (i >> lb)*sb + (i & (2^lb - 1))*si   (slab transpose buffers)
-// cs = 1 for y/x passes (columns are z), cs = L for z passes (columns are lines).
+// Element (o, i, z) lives at
+//   natural:  o*so + i*si + z
+//   peer:     o*so + (i >> lb)*sb + (i & (2^lb - 1))*si + z   (slab transpose buffers)
 struct Layout {
   uint32_t so, sb, si;
   int lb;
@@ -66,186 +194,56 @@ struct TileArgs {
   const double2* in;
   double2* out;
   Layout lin, lout;
-  uint32_t n_outer;     // number of outer indices
-  uint32_t nchunk;      // 8-column chunks per outer index
-  // potential phase (z passes)
-  const double* vi;     // v_i = (V - shift)/E0 at the same element offsets as psi
-  const double2* expv;  // exp(-i v_i dt_i) table (VTAB)
-  // kinetic phase (x pass)
-  const double* kx2;    // along the pass axis (length L)
-  const double* ky2;    // along the outer axis (global)
-  const double* kz2;    // along z
-  const double2* expk;  // exp(-i k^2 dt/2)/N table in the x-pass layout (KTAB)
-  uint32_t outer_off;   // global index of outer o = 0
-  double len2, dt_i;
-  double scale;         // folded inverse normalisation (power of two)
-  int imag;
+  uint32_t n_outer;  // number of outer indices
+  uint32_t nchunk;   // 8-column chunks per outer index (nz / 8)
+  PhaseArgs ph;
 };
 
-enum TileKind { T_FWD, T_INV, T_KIN, T_VFIRST, T_VMID, T_VLAST };
-
-// v[m] *= exp(i coef v_i dt) (real time) or exp(coef v_i dt) (imaginary time)
-__device__ __forceinline__ void mul_vphase(double2& v, double vi, double coef, const TileArgs& a) {
-  const double phi = v_phase_i(vi, coef, a.dt_i);
-  if (a.imag) {
-    const double f = exp(phi);
-    v = make_double2(v.x * f, v.y * f);
-  } else {
-    double s, c;
-    fast_sincos(phi, &s, &c);
-    v = cmul(v, make_double2(c, s));
-  }
-}
-
-// Cache policy (measured on B200, 512^3): the z passes stream through L2
-// only (an L1-allocated line would be hit again by the in-place store and
-// cost L1 data bandwidth); the strided passes keep the default policy.
-template <bool ZL>
-__device__ __forceinline__ double2 ld_psi(const double2* p) {
-  if constexpr (ZL) return __ldcg(p);
-  else return *p;
-}
-template <bool ZL>
-__device__ __forceinline__ void st_psi(double2* p, double2 v) {
-  if constexpr (ZL) __stcg(p, v);
-  else *p = v;
-}
-
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// Thread -> (line col, position t) of a tile.
-//   strided (y/x): col = lane & 7 (8 consecutive z), t = rest  -> 4 rows x 128 B per access
-//   contiguous (z): a warp covers TL consecutive t of 32/TL lines -> 4 rows x 128 B per access
-template <int L, bool ZL>
-struct TileMap {
-  int col, t, g;
-  __device__ __forceinline__ TileMap(int tid) {
-    using C = TileCfg<L>;
-    g = tid / C::per_tile;
-    const int r = tid - g * C::per_tile;
-    if constexpr (!ZL) {
-      col = r & 7;
-      t = r >> 3;
-    } else {
-      constexpr int TL = C::TL, CL = 32 / TL;           // lanes along the line / lines per warp
-      constexpr int WPL = (C::T / TL);                   // warps along one line group
-      const int lane = r & 31, w = r >> 5;
-      t = (w % WPL) * TL + (lane % TL);
-      col = (w / WPL) * CL + lane / TL;
+template <int L, int KIND, bool KTAB>
+__device__ __forceinline__ void tile_body(const TileArgs& a, double2* v, int t, uint32_t o, uint32_t z,
+                                          bool active, const double2* __restrict__ tw, SmemStrided sm) {
+  constexpr int T = L / kElems;
+  if constexpr (KIND == T_FWD) {
+    line_fft<L, -1>(v, t, tw, sm, SyncBlock{});
+  } else if constexpr (KIND == T_INV) {
+    line_fft<L, +1>(v, t, tw, sm, SyncBlock{});
+  } else {  // T_KIN: forward, K/N, inverse
+    line_fft<L, -1>(v, t, tw, sm, SyncBlock{});
+    if (active) {
+      if constexpr (KTAB) {
+#pragma unroll
+        for (int m = 0; m < kElems; ++m) v[m] = cmul(v[m], __ldcg(&a.ph.expk[lay<false>(a.lout, o, t + m * T) + z]));
+      } else {
+        const double ky2 = __ldg(&a.ph.ky2[a.ph.outer_off + o]);
+        const double kz2 = __ldg(&a.ph.kz2[z]);
+#pragma unroll
+        for (int m = 0; m < kElems; ++m) mul_kphase(v[m], __ldg(&a.ph.kx2[t + m * T]), ky2, kz2, a.ph);
+      }
     }
+    line_fft<L, +1>(v, t, tw, sm, SyncBlock{});
   }
-};
+}
 
-template <int L, int KIND, bool PIN, bool POUT, bool ZL, bool TAB>
-__global__ void __launch_bounds__(TileCfg<L>::threads, TileCfg<L>::minb) tile_kernel(TileArgs a,
+template <int L, int KIND, bool PIN, bool POUT, bool KTAB>
+__global__ void __launch_bounds__(TileCfg<L>::threads, KTAB ? TileCfg<L>::minb_tab : TileCfg<L>::minb) tile_kernel(TileArgs a,
                                                                                const double2* __restrict__ tw) {
   using C = TileCfg<L>;
-  constexpr uint32_t cs = ZL ? L : 1;
   extern __shared__ double2 smem[];
-  const TileMap<L, ZL> mp(threadIdx.x);
-  const int t = mp.t;
-  const uint32_t ntiles = a.n_outer * a.nchunk;
-  const uint32_t ngroups = (ntiles + C::G - 1) / C::G;
-
-  // persistent loop over tile groups; the next group is prefetched into L2
-  // while this one is in flight
-  for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const uint32_t nxt = grp + gridDim.x;
-    if (nxt < ngroups) {
-      const uint32_t ntile = nxt * C::G + mp.g;
-      if (ntile < ntiles) {
-        const uint32_t no = ntile / a.nchunk;
-        const uint32_t nco = (ntile - no * a.nchunk) * 8 * cs;
-        if constexpr (ZL) {
-          if ((threadIdx.x % C::per_tile) == 0) {
-            prefetch_l2_bulk(a.in + lay<false>(a.lin, no, 0) + nco, 8u * L * sizeof(double2));
-            if (KIND == T_VFIRST || KIND == T_VLAST || (KIND == T_VMID && !TAB))
-              prefetch_l2_bulk(a.vi + lay<false>(a.lin, no, 0) + nco, 8u * L * sizeof(double));
-            if (KIND == T_VMID && TAB)
-              prefetch_l2_bulk(a.expv + lay<false>(a.lin, no, 0) + nco, 8u * L * sizeof(double2));
-          }
-        } else {
-          const int row = threadIdx.x % C::per_tile;  // per_tile >= L rows of 128 B
-          if (row < L) {
-            prefetch_l2(a.in + lay<PIN>(a.lin, no, row) + nco);
-            if (KIND == T_KIN && TAB) prefetch_l2(a.expk + lay<false>(a.lout, no, row) + nco);
-          }
-        }
-      }
-    }
-    const uint32_t tile = grp * C::G + mp.g;
-    const bool active = tile < ntiles;
-    const uint32_t o = active ? tile / a.nchunk : 0;
-    const uint32_t cofs = ((active ? (tile - o * a.nchunk) : 0) * 8 + mp.col) * cs;
-
-    double2 v[kElems];
+  const int col = threadIdx.x & 7;
+  const int t = (threadIdx.x >> 3) % C::T;
+  const int g = threadIdx.x / C::per_tile;
+  const uint32_t tile = blockIdx.x * C::G + g;
+  const bool active = tile < a.n_outer * a.nchunk;
+  const uint32_t o = active ? tile / a.nchunk : 0;
+  const uint32_t z = (active ? (tile - o * a.nchunk) : 0) * 8 + col;
+  double2 v[kElems];
 #pragma unroll
-    for (int m = 0; m < kElems; ++m)
-      v[m] = active ? ld_psi<ZL>(&a.in[lay<PIN>(a.lin, o, t + m * C::T) + cofs]) : make_double2(0.0, 0.0);
-
-    auto body = [&](auto sm) {
-      if constexpr (KIND == T_FWD) {
-        line_fft<L, -1>(v, t, tw, sm, SyncBlock{});
-      } else if constexpr (KIND == T_INV) {
-        line_fft<L, +1>(v, t, tw, sm, SyncBlock{});
-      } else if constexpr (KIND == T_VFIRST) {  // Vh, then forward
-        if (active) {
+  for (int m = 0; m < kElems; ++m)
+    v[m] = active ? a.in[lay<PIN>(a.lin, o, t + m * C::T) + z] : make_double2(0.0, 0.0);
+  tile_body<L, KIND, KTAB>(a, v, t, o, z, active, tw, SmemStrided{smem + (size_t)g * L * 8 + col});
+  if (active) {
 #pragma unroll
-          for (int m = 0; m < kElems; ++m)
-            mul_vphase(v[m], __ldcg(&a.vi[lay<false>(a.lin, o, t + m * C::T) + cofs]), -0.5, a);
-        }
-        line_fft<L, -1>(v, t, tw, sm, SyncBlock{});
-      } else if constexpr (KIND == T_VMID || KIND == T_VLAST) {  // inverse, V (or Vh) [, forward]
-        line_fft<L, +1>(v, t, tw, sm, SyncBlock{});
-        if (active) {
-#pragma unroll
-          for (int m = 0; m < kElems; ++m) {
-            const uint32_t e = lay<false>(a.lin, o, t + m * C::T) + cofs;
-            if (KIND == T_VMID && TAB) v[m] = cmul(v[m], __ldcg(&a.expv[e]));
-            else mul_vphase(v[m], __ldcg(&a.vi[e]), KIND == T_VMID ? -1.0 : -0.5, a);
-          }
-        }
-        if constexpr (KIND == T_VMID) line_fft<L, -1>(v, t, tw, sm, SyncBlock{});
-      } else if constexpr (KIND == T_KIN) {  // forward, K/N, inverse
-        line_fft<L, -1>(v, t, tw, sm, SyncBlock{});
-        if (active) {
-          if constexpr (TAB) {
-#pragma unroll
-            for (int m = 0; m < kElems; ++m)
-              v[m] = cmul(v[m], __ldcg(&a.expk[lay<false>(a.lout, o, t + m * C::T) + cofs]));
-          } else {
-            const double ky2 = __ldg(&a.ky2[a.outer_off + o]);
-            const double kz2 = __ldg(&a.kz2[cofs]);
-#pragma unroll
-            for (int m = 0; m < kElems; ++m) {
-              const double phi = k_phase(__ldg(&a.kx2[t + m * C::T]), ky2, kz2, a.len2, a.dt_i);
-              if (a.imag) {
-                const double f = exp(phi) * a.scale;
-                v[m] = make_double2(v[m].x * f, v[m].y * f);
-              } else {
-                double s, c;
-                fast_sincos(phi, &s, &c);
-                v[m] = cmul(v[m], make_double2(c * a.scale, s * a.scale));
-              }
-            }
-          }
-        }
-        line_fft<L, +1>(v, t, tw, sm, SyncBlock{});
-      }
-    };
-    if constexpr (ZL) body(SmemContig{smem + ((size_t)mp.g * 8 + mp.col) * C::line_stride});
-    else body(SmemStrided{smem + (size_t)mp.g * L * 8 + mp.col});
-
-    if (active) {
-#pragma unroll
-      for (int m = 0; m < kElems; ++m) st_psi<ZL>(&a.out[lay<POUT>(a.lout, o, t + m * C::T) + cofs], v[m]);
-    }
-    __syncthreads();  // the exchange buffer is reused by the next group
+    for (int m = 0; m < kElems; ++m) a.out[lay<POUT>(a.lout, o, t + m * C::T) + z] = v[m];
   }
 }
 
@@ -253,41 +251,58 @@ __global__ void __launch_bounds__(TileCfg<L>::threads, TileCfg<L>::minb) tile_ke
 // host-side dispatch
 // ---------------------------------------------------------------------------
 
-template <int L, int KIND, bool PIN, bool POUT, bool ZL, bool TAB>
-static cudaError_t launch_tile(const TileArgs& a, const double2* tw, cudaStream_t st) {
-  using C = TileCfg<L>;
-  auto k = tile_kernel<L, KIND, PIN, POUT, ZL, TAB>;
-  static cudaError_t init =
-      C::smem > 48 * 1024 ? cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem)
-                          : cudaSuccess;
+template <typename K>
+static cudaError_t allow_smem(K k, size_t bytes) {
+  return bytes > 48 * 1024 ? cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)
+                           : cudaSuccess;
+}
+
+template <int L, int KIND, bool VTAB>
+static cudaError_t launch_z(const ZArgs& a, const double2* tw, cudaStream_t st) {
+  using C = ZCfg<L>;
+  auto k = zline_kernel<L, KIND, VTAB>;
+  static cudaError_t init = allow_smem(k, C::smem);
   if (init != cudaSuccess) return init;
-  static int max_blocks = [&] {
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C::threads, C::smem);
-    return sms * (per_sm > 0 ? per_sm : 1);
-  }();
-  const uint32_t ntiles = a.n_outer * a.nchunk;
-  const uint32_t groups = (ntiles + C::G - 1) / C::G;
-  const uint32_t blocks = groups < (uint32_t)max_blocks ? groups : (uint32_t)max_blocks;
-  k<<<blocks, C::threads, C::smem, st>>>(a, tw);
+  k<<<(a.nlines + C::C - 1) / C::C, C::threads, C::smem, st>>>(a, tw);
   return cudaGetLastError();
 }
 
-template <int KIND, bool PIN, bool POUT, bool ZL, bool TAB>
-static cudaError_t dispatch(int L, const TileArgs& a, const double2* tw, cudaStream_t st) {
-  switch (L) {
-    case 8: return launch_tile<8, KIND, PIN, POUT, ZL, TAB>(a, tw, st);
-    case 16: return launch_tile<16, KIND, PIN, POUT, ZL, TAB>(a, tw, st);
-    case 32: return launch_tile<32, KIND, PIN, POUT, ZL, TAB>(a, tw, st);
-    case 64: return launch_tile<64, KIND, PIN, POUT, ZL, TAB>(a, tw, st);
-    case 128: return launch_tile<128, KIND, PIN, POUT, ZL, TAB>(a, tw, st);
-    case 256: return launch_tile<256, KIND, PIN, POUT, ZL, TAB>(a, tw, st);
-    case 512: return launch_tile<512, KIND, PIN, POUT, ZL, TAB>(a, tw, st);
-    case 1024: return launch_tile<1024, KIND, PIN, POUT, ZL, TAB>(a, tw, st);
-  }
+template <int L, int KIND, bool PIN, bool POUT, bool KTAB>
+static cudaError_t launch_tile(const TileArgs& a, const double2* tw, cudaStream_t st) {
+  using C = TileCfg<L>;
+  auto k = tile_kernel<L, KIND, PIN, POUT, KTAB>;
+  static cudaError_t init = allow_smem(k, C::smem);
+  if (init != cudaSuccess) return init;
+  const uint32_t ntiles = a.n_outer * a.nchunk;
+  k<<<(ntiles + C::G - 1) / C::G, C::threads, C::smem, st>>>(a, tw);
+  return cudaGetLastError();
+}
+
+#define CTAP_BY_LENGTH(L, FN)                   \
+  switch (L) {                                  \
+    case 8: return FN(8);                       \
+    case 16: return FN(16);                     \
+    case 32: return FN(32);                     \
+    case 64: return FN(64);                     \
+    case 128: return FN(128);                   \
+    case 256: return FN(256);                   \
+    case 512: return FN(512);                   \
+    case 1024: return FN(1024);                 \
+  }                                             \
   return cudaErrorInvalidValue;
+
+template <int KIND, bool VTAB>
+static cudaError_t dispatch_z(int L, const ZArgs& a, const double2* tw, cudaStream_t st) {
+#define CTAP_Z(LL) launch_z<LL, KIND, VTAB>(a, tw, st)
+  CTAP_BY_LENGTH(L, CTAP_Z)
+#undef CTAP_Z
+}
+
+template <int KIND, bool PIN, bool POUT, bool KTAB>
+static cudaError_t dispatch_tile(int L, const TileArgs& a, const double2* tw, cudaStream_t st) {
+#define CTAP_T(LL) launch_tile<LL, KIND, PIN, POUT, KTAB>(a, tw, st)
+  CTAP_BY_LENGTH(L, CTAP_T)
+#undef CTAP_T
 }
 
 static int ilog2(int64_t v) {
@@ -362,44 +377,42 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
   const int64_t nx = p->n[0], ny = p->n[1], nz = p->n[2];
   const int P = p->slab_p;
   const uint32_t nxl = (uint32_t)(nx / P), nyl = (uint32_t)(ny / P);
-  TileArgs a;
-  a.in = (const double2*)in;
-  a.out = (double2*)out;
-  a.vi = p->vi_dev;
-  a.expv = p->expv_dev;
-  a.kx2 = p->k2_dev[0];
-  a.ky2 = p->k2_dev[1];
-  a.kz2 = p->k2_dev[2];
-  a.expk = p->expk_dev;
-  a.len2 = p->len2;
-  a.dt_i = p->dt_i;
-  a.scale = p->inv_scale;
-  a.imag = p->mode == 1;
-  a.outer_off = 0;
+  PhaseArgs ph;
+  ph.vi = p->vi_dev;
+  ph.expv = p->expv_dev;
+  ph.kx2 = p->k2_dev[0];
+  ph.ky2 = p->k2_dev[1];
+  ph.kz2 = p->k2_dev[2];
+  ph.expk = p->expk_dev;
+  ph.len2 = p->len2;
+  ph.dt_i = p->dt_i;
+  ph.scale = p->inv_scale;
+  ph.imag = p->mode == 1;
+  ph.outer_off = 0;
 
   if (kind >= PASS_Z_FWD && kind <= PASS_Z_LAST) {
     if (in != out) return cudaErrorInvalidValue;
-    // z-lines in groups of 8: element (o, i, col) at (8 o + col) L + i
-    const Layout zl{8u * (uint32_t)nz, 0u, 1u, 0};
-    a.lin = zl;
-    a.lout = zl;
-    a.n_outer = (uint32_t)(p->nx_local * ny / 8);
-    a.nchunk = 1;
+    ZArgs a;
+    a.psi = (double2*)out;
+    a.nlines = (uint32_t)(p->nx_local * ny);
+    a.ph = ph;
     const double2* tw = p->twiddles + (nz - 8);
     const int L = (int)nz;
-    const bool vtab = p->expv_dev != nullptr;
     switch (kind) {
-      case PASS_Z_FWD: return dispatch<T_FWD, false, false, true, false>(L, a, tw, st);
-      case PASS_Z_INV: return dispatch<T_INV, false, false, true, false>(L, a, tw, st);
-      case PASS_Z_FIRST: return dispatch<T_VFIRST, false, false, true, false>(L, a, tw, st);
+      case PASS_Z_FWD: return dispatch_z<T_FWD, false>(L, a, tw, st);
+      case PASS_Z_INV: return dispatch_z<T_INV, false>(L, a, tw, st);
+      case PASS_Z_FIRST: return dispatch_z<T_VFIRST, false>(L, a, tw, st);
       case PASS_Z_MID:
-        return vtab ? dispatch<T_VMID, false, false, true, true>(L, a, tw, st)
-                    : dispatch<T_VMID, false, false, true, false>(L, a, tw, st);
-      case PASS_Z_LAST: return dispatch<T_VLAST, false, false, true, false>(L, a, tw, st);
+        return p->expv_dev ? dispatch_z<T_VMID, true>(L, a, tw, st) : dispatch_z<T_VMID, false>(L, a, tw, st);
+      case PASS_Z_LAST: return dispatch_z<T_VLAST, false>(L, a, tw, st);
     }
     return cudaErrorInvalidValue;
   }
+  TileArgs a;
+  a.in = (const double2*)in;
+  a.out = (double2*)out;
   a.nchunk = (uint32_t)(nz / 8);
+  a.ph = ph;
   // natural x-slab layout (x_local, y, z), lines along y
   const Layout y_nat{(uint32_t)(ny * nz), 0u, (uint32_t)nz, 0};
   // peer-major layout [peer][x_local][y_local][z] for the y <-> x transposes
@@ -416,18 +429,18 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       if (kind == PASS_Y_FWD_TO_PEER && peer) {
         a.lin = y_nat;
         a.lout = y_peer;
-        return dispatch<T_FWD, false, true, false, false>(L, a, tw, st);
+        return dispatch_tile<T_FWD, false, true, false>(L, a, tw, st);
       }
       if (kind == PASS_Y_INV_FROM_PEER && peer) {
         a.lin = y_peer;
         a.lout = y_nat;
-        return dispatch<T_INV, true, false, false, false>(L, a, tw, st);
+        return dispatch_tile<T_INV, true, false, false>(L, a, tw, st);
       }
       a.lin = y_nat;
       a.lout = y_nat;
       const bool fwd = (kind == PASS_Y_FWD || kind == PASS_Y_FWD_TO_PEER);
-      return fwd ? dispatch<T_FWD, false, false, false, false>(L, a, tw, st)
-                 : dispatch<T_INV, false, false, false, false>(L, a, tw, st);
+      return fwd ? dispatch_tile<T_FWD, false, false, false>(L, a, tw, st)
+                 : dispatch_tile<T_INV, false, false, false>(L, a, tw, st);
     }
     case PASS_X_KIN:
     case PASS_X_FWD:
@@ -437,14 +450,14 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       a.lin = x_nat;
       a.lout = x_nat;
       a.n_outer = nyl;
-      a.outer_off = (uint32_t)p->slab_r * nyl;
+      a.ph.outer_off = (uint32_t)p->slab_r * nyl;
       const double2* tw = p->twiddles + (nx - 8);
       const int L = (int)nx;
       if (kind == PASS_X_KIN)
-        return p->expk_dev ? dispatch<T_KIN, false, false, false, true>(L, a, tw, st)
-                           : dispatch<T_KIN, false, false, false, false>(L, a, tw, st);
-      if (kind == PASS_X_FWD) return dispatch<T_FWD, false, false, false, false>(L, a, tw, st);
-      return dispatch<T_INV, false, false, false, false>(L, a, tw, st);
+        return p->expk_dev ? dispatch_tile<T_KIN, false, false, true>(L, a, tw, st)
+                           : dispatch_tile<T_KIN, false, false, false>(L, a, tw, st);
+      if (kind == PASS_X_FWD) return dispatch_tile<T_FWD, false, false, false>(L, a, tw, st);
+      return dispatch_tile<T_INV, false, false, false>(L, a, tw, st);
     }
   }
   return cudaErrorInvalidValue;

@@ -32,9 +32,12 @@ from .qgrid import UnitSystem, Wavefunction, as_simgrid, grid_key, same_grid, wr
 REAL_TIME = "real_time"
 IMAGINARY_TIME = "imaginary_time"
 
-# default phase mode of make_plan; the
-# environment variable is for A/B measurements
-DEFAULT_PHASE_TABLES = os.environ.get("CTAP_PHASE_TABLES", "0") == "1"
+# phase-table mask of make_plan (bit 0: exp(-iV dt) table, bit 1: exp(-ik^2 dt/2)
+# table); the environment variable is for A/B
+# measurements
+PHASE_TABLE_V = 1
+PHASE_TABLE_K = 2
+DEFAULT_PHASE_TABLES = int(os.environ.get("CTAP_PHASE_TABLES", str(PHASE_TABLE_V)))
 
 
 class ConvergenceError(RuntimeError):
@@ -50,7 +53,7 @@ class NativePlan:
 
     def __init__(self, grid, v_dev: torch.Tensor | None, mass: float, dt: float,
                  mode: str = REAL_TIME, v_shift: float = 0.0, slab_p: int = 1, slab_r: int = 0,
-                 phase_tables: bool = False):
+                 phase_tables: int = 0):
         lib = _lib.load()
         dev = _device.require_cuda()
         self.grid = as_simgrid(grid)
@@ -65,15 +68,16 @@ class NativePlan:
         desc.mode = _lib.REAL_TIME_MODE if mode == REAL_TIME else _lib.IMAGINARY_TIME_MODE
         desc.slab_p = int(slab_p)
         desc.slab_r = int(slab_r)
-        desc.phase_tables = int(bool(phase_tables))
+        desc.phase_tables = int(phase_tables)
         self.desc = desc
         # squared wavenumbers exactly as k_squared() forms them (qgrid.py:112-115)
         self._k2 = [np.ascontiguousarray(self.grid.k_axis(i) ** 2) for i in range(3)]
-        self._v = v_dev if v_dev is not None else torch.zeros(1, dtype=torch.float64, device=dev)
+        self._v = v_dev  # None: FFT/reduction-only plan
         handle = ctypes.c_void_p()
         _lib.check(lib.ctap_plan_create(ctypes.byref(desc), self._k2[0].ctypes.data,
                                         self._k2[1].ctypes.data, self._k2[2].ctypes.data,
-                                        self._v.data_ptr(), ctypes.byref(handle)))
+                                        None if v_dev is None else v_dev.data_ptr(),
+                                        ctypes.byref(handle)))
         self.handle = handle
         self._fin = weakref.finalize(self, lib.ctap_plan_destroy, handle)
         self._out = torch.zeros(8, dtype=torch.float64, device=dev)
@@ -117,7 +121,7 @@ class NativePlan:
     def phase_field(self, which: int) -> torch.Tensor:
         nxl = self.grid.n[0] // self.desc.slab_p
         out = torch.empty((nxl, self.grid.n[1], self.grid.n[2]), dtype=torch.complex128,
-                          device=self._v.device)
+                          device=self._out.device)
         _lib.call("ctap_phase_field", self.handle, int(which), out.data_ptr(), _device.stream_handle())
         return out
 
@@ -179,13 +183,15 @@ class StepPlan:
 
 
 def make_plan(grid, potential, mass: float, dt: float, mode: str = REAL_TIME,
-              threads: int = 1, *, phase_tables: bool | None = None) -> StepPlan:
+              threads: int = 1, *, phase_tables: int | None = None) -> StepPlan:
     """make_plan (propagator.py:55-81).
 
     `threads` is accepted for signature compatibility (the device decides its
-    own parallelism).  `phase_tables` (B200 extension) keeps exp(-i V dt) and
-    exp(-i k^2 dt/2) as HBM tables instead of recomputing them per step; the
-    phases are bit-identical either way.  None picks the faster mode."""
+    own parallelism).  `phase_tables` (B200 extension) is a mask choosing
+    which of exp(-i V dt) (PHASE_TABLE_V) and exp(-i k^2 dt/2)
+    (PHASE_TABLE_K) are kept as HBM tables instead of being recomputed per
+    point every step; the phases are bit-identical either way.  None picks
+    the measured-fastest default."""
     if mode not in (REAL_TIME, IMAGINARY_TIME):
         raise ValueError(f"unknown mode {mode!r}")
     if tuple(potential.shape) != tuple(grid.n):

@@ -1,0 +1,165 @@
+"""x-slab domain decomposition of the split-step propagator over several GPUs
+(one process per GPU, torch.distributed over NCCL / NVLink).
+
+Rank r of P owns the x-planes [r*nx/P, (r+1)*nx/P) of psi and V (both
+contiguous slabs).  The z and y transforms are local; the x transform needs
+whole x-lines, so every step transposes twice:
+
+    [z^-1 V z]  ->  y (output written peer-major)  -> all-to-all
+    -> [x K x^-1] on the y-slab (x, y_local, z)     -> all-to-all
+    -> y^-1 (input read peer-major)                 -> next step
+
+The y passes write/read the all-to-all buffers directly in peer-major order
+([peer][x_local][y_local][z]), so no pack/unpack sweep exists, and the
+receive buffer of the first all-to-all is already the natural y-slab layout
+the x pass runs on.  Observer sums are per-rank partials combined in rank
+order on every rank (deterministic, no float atomics).
+
+The schedule (SlabSchedule) is independent of the compute backend so the
+same code drives the CUDA passes here and the CPU emulation in the gloo
+tests (tests/test_slab_gloo.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _device, _lib
+from .propagator import REAL_TIME, NativePlan
+from .qgrid import as_simgrid
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    """Sizes of the x-slab / y-slab decomposition of an (nx, ny, nz) grid."""
+
+    n: tuple
+    P: int
+    rank: int
+
+    def __post_init__(self):
+        nx, ny, _ = self.n
+        if nx % self.P or ny % self.P:
+            raise ValueError(f"nx={nx} and ny={ny} must be divisible by {self.P} ranks")
+        if not 0 <= self.rank < self.P:
+            raise ValueError(f"rank {self.rank} out of range for {self.P} ranks")
+
+    @property
+    def nx_local(self) -> int:
+        return self.n[0] // self.P
+
+    @property
+    def ny_local(self) -> int:
+        return self.n[1] // self.P
+
+    @property
+    def x_slice(self) -> slice:
+        return slice(self.rank * self.nx_local, (self.rank + 1) * self.nx_local)
+
+    @property
+    def y_slice(self) -> slice:
+        return slice(self.rank * self.ny_local, (self.rank + 1) * self.ny_local)
+
+    @property
+    def slab_shape(self) -> tuple:      # position-space x-slab
+        return (self.nx_local, self.n[1], self.n[2])
+
+    @property
+    def yslab_shape(self) -> tuple:     # x-pass y-slab
+        return (self.n[0], self.ny_local, self.n[2])
+
+    @property
+    def points(self) -> int:
+        return self.nx_local * self.n[1] * self.n[2]
+
+    def a2a_bytes_per_step(self, itemsize: int = 16) -> int:
+        """Bytes this rank sends over NVLink per split step (2 transposes)."""
+        return 2 * (self.P - 1) * self.points // self.P * itemsize
+
+
+# pass sequence of one telescoped segment (propagator.py:98-107)
+def segment_schedule(n_steps: int):
+    """Yield the operations of n merged steps on one rank:
+    ('pass', kind, src, dst) with buffer names 'psi' / 'send' / 'recv', and
+    ('a2a', src, dst)."""
+    if n_steps <= 0:
+        return
+    yield ("pass", _lib.PASS_Z_FIRST, "psi", "psi")
+    for j in range(n_steps):
+        yield ("pass", _lib.PASS_Y_FWD_TO_PEER, "psi", "send")
+        yield ("a2a", "send", "recv")
+        yield ("pass", _lib.PASS_X_KIN, "recv", "recv")
+        yield ("a2a", "recv", "send")
+        yield ("pass", _lib.PASS_Y_INV_FROM_PEER, "send", "psi")
+        yield ("pass", _lib.PASS_Z_MID if j < n_steps - 1 else _lib.PASS_Z_LAST, "psi", "psi")
+
+
+def combine_in_rank_order(local: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum per-rank partial sums in rank order (bitwise identical on every rank)."""
+    P = dist.get_world_size(group)
+    parts = [torch.empty_like(local) for _ in range(P)]
+    dist.all_gather(parts, local, group=group)
+    total = parts[0].clone()
+    for p in parts[1:]:
+        total += p
+    return total
+
+
+class SlabPropagator:
+    """Real- or imaginary-time propagation of one rank's x-slab on its GPU."""
+
+    def __init__(self, grid, v_local, mass: float, dt: float, group=None, mode: str = REAL_TIME,
+                 v_shift: float = 0.0, phase_tables: int | None = None):
+        self.grid = as_simgrid(grid)
+        self.group = group
+        P = dist.get_world_size(group) if dist.is_initialized() else 1
+        r = dist.get_rank(group) if dist.is_initialized() else 0
+        self.layout = SlabLayout(tuple(self.grid.n), P, r)
+        if tuple(v_local.shape) != self.layout.slab_shape:
+            raise ValueError(f"local potential shape {tuple(v_local.shape)} != slab {self.layout.slab_shape}")
+        self.v_local = _device.to_device_f64(v_local)
+        from .propagator import DEFAULT_PHASE_TABLES
+
+        if phase_tables is None:
+            phase_tables = DEFAULT_PHASE_TABLES
+        self.phase_tables = int(phase_tables)
+        self.native = NativePlan(self.grid, self.v_local, mass, dt, mode, v_shift=v_shift,
+                                 slab_p=P, slab_r=r, phase_tables=phase_tables)
+        dev = self.v_local.device
+        self.send = torch.empty(self.layout.points, dtype=torch.complex128, device=dev)
+        self.recv = torch.empty(self.layout.points, dtype=torch.complex128, device=dev)
+
+    def _a2a(self, src: torch.Tensor, dst: torch.Tensor):
+        if self.layout.P == 1:
+            dst.copy_(src)
+        else:
+            dist.all_to_all_single(torch.view_as_real(dst), torch.view_as_real(src), group=self.group)
+
+    def advance(self, psi_local: torch.Tensor, n_steps: int):
+        """n telescoped steps on this rank's slab (collective: all ranks call)."""
+        if n_steps < 0:
+            raise ValueError("n_steps must be >= 0")
+        if self.layout.P == 1:
+            self.native.advance(psi_local, n_steps)
+            return
+        bufs = {"psi": psi_local.reshape(-1), "send": self.send, "recv": self.recv}
+        for op in segment_schedule(n_steps):
+            if op[0] == "pass":
+                _, kind, src, dst = op
+                self.native.run_pass(kind, bufs[src], bufs[dst])
+            else:
+                self._a2a(bufs[op[1]], bufs[op[2]])
+
+    def observe(self, psi_local: torch.Tensor, xb1=None, xb2=None, margin: int = 2) -> list:
+        """Global [sum rho, left, middle, right, edge] (raw sums, rank-ordered)."""
+        xs = _device.to_device_f64(self.grid.x[self.layout.x_slice])
+        b1 = None if xb1 is None else _device.to_device_f64(np.asarray(xb1))
+        b2 = None if xb2 is None else _device.to_device_f64(np.asarray(xb2))
+        local = self.native.observe(psi_local, xs, b1, b2, margin)
+        if self.layout.P == 1:
+            return local.tolist()
+        return combine_in_rank_order(local, self.group).tolist()

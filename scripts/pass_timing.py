@@ -24,7 +24,7 @@ def main():
     n = nx * ny * nz
     v = torch.full((nx, ny, nz), muB / 2 * 0.03, dtype=torch.float64, device="cuda")
     v += torch.rand_like(v) * 1e-29
-    plan = propagator.make_plan(grid, v, m, 1e-6)
+    plan = propagator.make_plan(grid, v, m, 1e-6, phase_tables=int(os.environ.get('CTAP_PHASE_TABLES', '1')))
     psi = (torch.randn(nx, ny, nz, dtype=torch.complex128, device="cuda") * 1e-3).contiguous()
     P = _lib
     passes = [("Z_MID", P.PASS_Z_MID, 40), ("Y_FWD", P.PASS_Y_FWD, 32), ("X_KIN", P.PASS_X_KIN, 32),
