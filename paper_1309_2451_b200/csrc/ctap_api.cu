@@ -40,21 +40,6 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 bool pow2_in_range(int64_t n) { return n >= 8 && n <= 1024 && (n & (n - 1)) == 0; }
 
-// exp(-2 pi i m / L) for L = 8..1024, concatenated (table for L at offset L-8),
-// evaluated in extended precision so every entry is the correctly rounded
-// double (the FFT round-off budget relies on ~1-ulp twiddles).
-std::vector<double> make_twiddles() {
-  std::vector<double> t;
-  for (int L = 8; L <= 1024; L *= 2) {
-    for (int m = 0; m < L; ++m) {
-      long double ang = 2.0L * 3.14159265358979323846264338327950288L * (long double)m / (long double)L;
-      t.push_back((double)cosl(ang));
-      t.push_back((double)(-sinl(ang)));
-    }
-  }
-  return t;
-}
-
 }  // namespace
 
 #define CUDA_TRY(expr, what)                       \
@@ -102,7 +87,7 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
     e = cudaMalloc((void**)&p->k2_dev[i], sizeof(double) * d->n[i]);
     if (e == cudaSuccess) e = cudaMemcpy(p->k2_dev[i], k2h[i], sizeof(double) * d->n[i], cudaMemcpyHostToDevice);
   }
-  std::vector<double> tw = make_twiddles();
+  std::vector<double> tw = ctap_make_twiddles(p->tw_off);
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->twiddles, tw.size() * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(p->twiddles, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice);
   int dev = 0, sms = 148;

@@ -113,6 +113,16 @@ struct Plan {
     for (int i = 0; i < s; ++i) p *= radix(i);
     return p;
   }
+  // Stage-major twiddle table: stage s >= 1 holds (R_s - 1) x NS_s entries
+  // T[r-1][k] = exp(-2 pi i r k / (NS_s R_s)); for a fixed r the k of a warp
+  // are consecutive, so a twiddle gather touches as few 128-byte lines as the
+  // data access does.
+  __host__ __device__ static constexpr int tw_offset(int s) {
+    int o = 0;
+    for (int i = 1; i < s; ++i) o += (radix(i) - 1) * ns(i);
+    return o;
+  }
+  static constexpr int tw_size = tw_offset(nstages);
 };
 
 // Contiguous-line shared-memory position with one 16-byte pad every 8 points
@@ -148,7 +158,7 @@ struct SyncNamed {  // T threads (a multiple of 32) of one line: named barrier
 //   radix R, stride Ns (product of earlier radices), line length L.
 // Input: v[m] = x[t + m*T].  Output scattered to smem (unless last stage, in
 // which case v[m] = X[t + m*T] stays in registers).
-template <int L, int R, int NS, int DIR, bool LAST, typename Smem>
+template <int L, int R, int NS, int TWO, int DIR, bool LAST, typename Smem>
 __device__ __forceinline__ void stockham_stage(double2* v, int t, const double2* __restrict__ tw, Smem sm) {
   constexpr int T = L / kElems;
   constexpr int NB = kElems / R;  // butterflies per thread
@@ -160,11 +170,10 @@ __device__ __forceinline__ void stockham_stage(double2* v, int t, const double2*
     const int j = t + b * T;
     const int k = j & (NS - 1);
     if (NS > 1) {
-      // twiddle exp(DIR 2 pi i r k / (NS R)) = W_L^(r k L/(NS R))
-      constexpr int step = L / (NS * R);
+      // twiddle exp(DIR 2 pi i r k / (NS R)) from the stage-major table
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        double2 w = __ldg(&tw[r * k * step]);
+        double2 w = __ldg(&tw[TWO + (r - 1) * NS + k]);
         u[r] = DIR < 0 ? cmul(u[r], w) : cmulc(u[r], w);
       }
     }
@@ -189,7 +198,7 @@ __device__ __forceinline__ void fft_stages(double2* v, int t, const double2* __r
     constexpr int R = P::radix(S);
     constexpr int NS = P::ns(S);
     constexpr bool LAST = (S == P::nstages - 1);
-    stockham_stage<L, R, NS, DIR, LAST>(v, t, tw, sm);
+    stockham_stage<L, R, NS, P::tw_offset(S), DIR, LAST>(v, t, tw, sm);
     if constexpr (!LAST) {
       sync();
 #pragma unroll

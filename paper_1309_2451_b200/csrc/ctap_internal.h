@@ -42,11 +42,14 @@ struct ctap_plan {
   double2* expv_dev;       // optional table exp(-i v_i dt_i)       (phase_tables, real time)
   double2* expk_dev;       // optional table exp(-i k^2 dt/2) / N, x-pass layout
   double* k2_dev[3];       // squared wavenumbers per axis (global lengths)
-  double2* twiddles;       // concatenated exp(-2 pi i m / L), L = 8..1024
+  double2* twiddles;       // stage-major twiddle tables for L = 8..1024
+  int tw_off[8];           // start of the table of L = 8 << i
   double* red_partial;     // reduction scratch
   int red_blocks;
 };
 
 cudaError_t ctap_run_v_internal(const ctap_plan* p, cudaStream_t st);
 cudaError_t ctap_run_phase_field(const ctap_plan* p, int which, void* out, cudaStream_t st);
+#include <vector>
+std::vector<double> ctap_make_twiddles(int off[8]);
 cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* out, cudaStream_t st);

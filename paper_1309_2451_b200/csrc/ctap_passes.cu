@@ -23,6 +23,9 @@
 // 8 B/pt of v_i = V/E0 per step) or from plan-owned complex tables of the
 // same values (16 B/pt for the full V step and for K, no sincos per step);
 // both give bit-identical phases.
+#include <cmath>
+#include <vector>
+
 #include "ctap_device.cuh"
 #include "ctap_internal.h"
 
@@ -343,9 +346,40 @@ __global__ void v_internal_kernel(const double* __restrict__ V, double* __restri
     vi[i] = v_internal(V[i], shift, e0);
 }
 
+template <int L>
+static void append_stage_twiddles(std::vector<double>& t) {
+  using P = Plan<L>;
+  for (int s = 1; s < P::nstages; ++s) {
+    const int R = P::radix(s), NS = P::ns(s);
+    for (int r = 1; r < R; ++r)
+      for (int k = 0; k < NS; ++k) {
+        // extended precision so every entry is the correctly rounded double
+        const long double ang = 2.0L * 3.14159265358979323846264338327950288L * (long double)(r * k) /
+                                (long double)(NS * R);
+        t.push_back((double)cosl(ang));
+        t.push_back((double)(-sinl(ang)));
+      }
+  }
+}
+
 }  // namespace ctap
 
 using namespace ctap;
+
+// all stage-major twiddle tables, L = 8..1024; off[i] = start (in double2) of L = 8 << i
+std::vector<double> ctap_make_twiddles(int off[8]) {
+  std::vector<double> t;
+  off[0] = (int)(t.size() / 2); append_stage_twiddles<8>(t);
+  off[1] = (int)(t.size() / 2); append_stage_twiddles<16>(t);
+  off[2] = (int)(t.size() / 2); append_stage_twiddles<32>(t);
+  off[3] = (int)(t.size() / 2); append_stage_twiddles<64>(t);
+  off[4] = (int)(t.size() / 2); append_stage_twiddles<128>(t);
+  off[5] = (int)(t.size() / 2); append_stage_twiddles<256>(t);
+  off[6] = (int)(t.size() / 2); append_stage_twiddles<512>(t);
+  off[7] = (int)(t.size() / 2); append_stage_twiddles<1024>(t);
+  if (t.empty()) t.assign(2, 0.0);
+  return t;
+}
 
 cudaError_t ctap_run_v_internal(const ctap_plan* p, cudaStream_t st) {
   const uint32_t n = (uint32_t)(p->nx_local * p->n[1] * p->n[2]);
@@ -396,7 +430,7 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
     a.psi = (double2*)out;
     a.nlines = (uint32_t)(p->nx_local * ny);
     a.ph = ph;
-    const double2* tw = p->twiddles + (nz - 8);
+    const double2* tw = p->twiddles + p->tw_off[ilog2(nz) - 3];
     const int L = (int)nz;
     switch (kind) {
       case PASS_Z_FWD: return dispatch_z<T_FWD, false>(L, a, tw, st);
@@ -424,7 +458,7 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
     case PASS_Y_FWD_TO_PEER:
     case PASS_Y_INV_FROM_PEER: {
       a.n_outer = nxl;
-      const double2* tw = p->twiddles + (ny - 8);
+      const double2* tw = p->twiddles + p->tw_off[ilog2(ny) - 3];
       const int L = (int)ny;
       if (kind == PASS_Y_FWD_TO_PEER && peer) {
         a.lin = y_nat;
@@ -451,7 +485,7 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       a.lout = x_nat;
       a.n_outer = nyl;
       a.ph.outer_off = (uint32_t)p->slab_r * nyl;
-      const double2* tw = p->twiddles + (nx - 8);
+      const double2* tw = p->twiddles + p->tw_off[ilog2(nx) - 3];
       const int L = (int)nx;
       if (kind == PASS_X_KIN)
         return p->expk_dev ? dispatch_tile<T_KIN, false, false, true>(L, a, tw, st)
