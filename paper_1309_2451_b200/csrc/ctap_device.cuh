@@ -26,12 +26,15 @@ constexpr int kElems = 8;  // points per thread per line
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// complex products with an explicit FMA pattern, so the rounding does not
+// depend on how the compiler contracts the surrounding code (keeps e.g. the
+// slab and single-GPU paths bitwise identical)
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  return make_double2(fma(a.x, b.x, -__dmul_rn(a.y, b.y)), fma(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
 // a * conj(b)
 __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
-  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+  return make_double2(fma(a.x, b.x, __dmul_rn(a.y, b.y)), fma(a.y, b.x, -__dmul_rn(a.x, b.y)));
 }
 // multiply by -i (DIR=-1, forward) or +i (DIR=+1, inverse)
 template <int DIR>

@@ -120,15 +120,23 @@ __device__ __forceinline__ void z_body(const ZArgs& a, double2* v, int t, uint32
       for (int m = 0; m < kElems; ++m) mul_vphase(v[m], __ldcg(&a.ph.vi[off + t + m * T]), -0.5, a.ph);
     }
     line_fft<L, -1>(v, t, tw, sm, sync);
-  } else {  // T_VMID: inverse, V, forward; T_VLAST: inverse, Vh
-    line_fft<L, +1>(v, t, tw, sm, sync);
-    if (active) {
+  } else if constexpr (KIND == T_VMID && VTAB) {  // inverse, x exp(-iV dt) table, forward
+    // the table values are loaded before the inverse transform so their
+    // latency hides behind it (they are consumed right after it)
+    double2 f[kElems];
 #pragma unroll
-      for (int m = 0; m < kElems; ++m) {
-        if (KIND == T_VMID && VTAB) v[m] = cmul(v[m], __ldcg(&a.ph.expv[off + t + m * T]));
-        else mul_vphase(v[m], __ldcg(&a.ph.vi[off + t + m * T]), KIND == T_VMID ? -1.0 : -0.5, a.ph);
-      }
-    }
+    for (int m = 0; m < kElems; ++m) f[m] = active ? __ldcg(&a.ph.expv[off + t + m * T]) : make_double2(1.0, 0.0);
+    line_fft<L, +1>(v, t, tw, sm, sync);
+#pragma unroll
+    for (int m = 0; m < kElems; ++m) v[m] = cmul(v[m], f[m]);
+    line_fft<L, -1>(v, t, tw, sm, sync);
+  } else {  // T_VMID: inverse, V, forward; T_VLAST: inverse, Vh
+    double vi[kElems];
+#pragma unroll
+    for (int m = 0; m < kElems; ++m) vi[m] = active ? __ldcg(&a.ph.vi[off + t + m * T]) : 0.0;
+    line_fft<L, +1>(v, t, tw, sm, sync);
+#pragma unroll
+    for (int m = 0; m < kElems; ++m) mul_vphase(v[m], vi[m], KIND == T_VMID ? -1.0 : -0.5, a.ph);
     if constexpr (KIND == T_VMID) line_fft<L, -1>(v, t, tw, sm, sync);
   }
 }
@@ -211,16 +219,21 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, double2* v, int t, 
   } else if constexpr (KIND == T_INV) {
     line_fft<L, +1>(v, t, tw, sm, SyncBlock{});
   } else {  // T_KIN: forward, K/N, inverse
+    double kx2[kElems], ky2 = 0.0, kz2 = 0.0;
+    if constexpr (!KTAB) {  // operands of the phase, loaded ahead of the forward transform
+      ky2 = __ldg(&a.ph.ky2[a.ph.outer_off + o]);
+      kz2 = __ldg(&a.ph.kz2[z]);
+#pragma unroll
+      for (int m = 0; m < kElems; ++m) kx2[m] = __ldg(&a.ph.kx2[t + m * T]);
+    }
     line_fft<L, -1>(v, t, tw, sm, SyncBlock{});
     if (active) {
       if constexpr (KTAB) {
 #pragma unroll
         for (int m = 0; m < kElems; ++m) v[m] = cmul(v[m], __ldcg(&a.ph.expk[lay<false>(a.lout, o, t + m * T) + z]));
       } else {
-        const double ky2 = __ldg(&a.ph.ky2[a.ph.outer_off + o]);
-        const double kz2 = __ldg(&a.ph.kz2[z]);
 #pragma unroll
-        for (int m = 0; m < kElems; ++m) mul_kphase(v[m], __ldg(&a.ph.kx2[t + m * T]), ky2, kz2, a.ph);
+        for (int m = 0; m < kElems; ++m) mul_kphase(v[m], kx2[m], ky2, kz2, a.ph);
       }
     }
     line_fft<L, +1>(v, t, tw, sm, SyncBlock{});

@@ -33,10 +33,10 @@ def _case(n=(32, 16, 32)):
     return grid, v, a0
 
 
-def run_virtual(grid, v, a0, P, steps):
+def run_virtual(grid, v, a0, P, steps, tables=0):
     lays = [SlabLayout(grid.n, P, r) for r in range(P)]
     vs = [torch.from_numpy(np.ascontiguousarray(v[l.x_slice])).cuda() for l in lays]
-    plans = [NativePlan(grid, vs[r], M, 1e-6, slab_p=P, slab_r=r) for r in range(P)]
+    plans = [NativePlan(grid, vs[r], M, 1e-6, slab_p=P, slab_r=r, phase_tables=tables) for r in range(P)]
     bufs = [{"psi": torch.from_numpy(np.ascontiguousarray(a0[l.x_slice])).cuda().reshape(-1),
              "send": torch.empty(l.points, dtype=torch.complex128, device="cuda"),
              "recv": torch.empty(l.points, dtype=torch.complex128, device="cuda")} for l in lays]
@@ -54,12 +54,12 @@ def run_virtual(grid, v, a0, P, steps):
     return out.cpu().numpy(), plans, bufs, lays
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
-def test_virtual_slabs_bitwise_equal_single_gpu(P):
+@pytest.mark.parametrize("P,tables", [(2, 0), (4, 0), (8, 0), (2, 1), (4, 3)])
+def test_virtual_slabs_bitwise_equal_single_gpu(P, tables):
     grid, v, a0 = _case()
-    got, *_ = run_virtual(grid, v, a0, P, 6)
+    got, *_ = run_virtual(grid, v, a0, P, 6, tables)
     psi = qgrid.Wavefunction(a0.copy(), grid)
-    plan = propagator.make_plan(grid, v, M, 1e-6)
+    plan = propagator.make_plan(grid, v, M, 1e-6, phase_tables=tables)
     psi, _ = propagator.evolve_real(psi, plan, 6)
     assert np.array_equal(got, psi.amplitudes)
 
