@@ -59,7 +59,12 @@ typedef enum ctap_pass_kind {
   CTAP_PASS_Y_INV_FROM_PEER = 8, /* input in peer-major receive layout, y^-1 */
   CTAP_PASS_X_KIN = 9,    /* psi <- Fx^-1 (K/N) Fx psi on the y-slab layout */
   CTAP_PASS_X_FWD = 10,
-  CTAP_PASS_X_INV = 11
+  CTAP_PASS_X_INV = 11,
+  /* single-GPU step on the blocked k-space layout (out of place y passes):
+   * B(x, y, z) = ((x >> lx) ny + y) 2^lx nz + (x & (2^lx - 1)) nz + z */
+  CTAP_PASS_Y_FWD_BLK = 12,  /* y FFT, natural psi -> blocked buffer */
+  CTAP_PASS_X_KIN_BLK = 13,  /* [x K x^-1] on the blocked buffer, in place */
+  CTAP_PASS_Y_INV_BLK = 14   /* y^-1, blocked buffer -> natural psi */
 } ctap_pass_kind;
 
 typedef struct ctap_plan ctap_plan;

@@ -26,6 +26,7 @@ IMAGINARY_TIME_MODE = 1
 PASS_Z_FWD, PASS_Z_INV, PASS_Z_FIRST, PASS_Z_MID, PASS_Z_LAST = range(5)
 PASS_Y_FWD, PASS_Y_INV, PASS_Y_FWD_TO_PEER, PASS_Y_INV_FROM_PEER = range(5, 9)
 PASS_X_KIN, PASS_X_FWD, PASS_X_INV = range(9, 12)
+PASS_Y_FWD_BLK, PASS_X_KIN_BLK, PASS_Y_INV_BLK = range(12, 15)
 
 # every symbol include/ctap.h declares
 EXPORTS = (

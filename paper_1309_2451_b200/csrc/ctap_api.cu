@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -96,6 +97,18 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   p->red_blocks = sms * 4;
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->red_partial, sizeof(double) * 8 * p->red_blocks);
   const size_t nloc = (size_t)p->nx_local * d->n[1] * d->n[2];
+  // single GPU, opt-in (CTAP_KBLK_LX=lx > 0): out-of-place y passes into a
+  // blocked k-space buffer so an x-line spans nx/2^lx address blocks instead of
+  // nx.  Measured slower than the in-place natural layout on B200 at 512^3
+  // (DESIGN.md §3), hence off by default.
+  p->k_lx = 0;
+  if (P == 1 && v_dev && d->n[0] >= 16) {
+    int lx = 0;
+    if (const char* env = getenv("CTAP_KBLK_LX")) lx = atoi(env);
+    while (lx > 0 && (int64_t(1) << lx) > d->n[0]) --lx;
+    p->k_lx = lx < 0 ? 0 : lx;
+    if (p->k_lx > 0 && e == cudaSuccess) e = cudaMalloc((void**)&p->kbuf, sizeof(double2) * nloc);
+  }
   if (v_dev) {  // a plan without a potential only serves FFTs and reductions
     if (e == cudaSuccess) e = cudaMalloc((void**)&p->vi_dev, sizeof(double) * nloc);
     if (e == cudaSuccess) e = ctap_run_v_internal(p, 0);
@@ -125,13 +138,17 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
   cudaFree(p->vi_dev);
   cudaFree(p->expv_dev);
   cudaFree(p->expk_dev);
+  cudaFree(p->kbuf);
   delete p;
   return CTAP_OK;
 }
 
 CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, void* stream) {
   if (!p || !in || !out) return fail(CTAP_EINVAL, "null argument");
-  if (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_X_INV) return fail(CTAP_EINVAL, "unknown pass %d", kind);
+  if (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_Y_INV_BLK) return fail(CTAP_EINVAL, "unknown pass %d", kind);
+  if (kind >= CTAP_PASS_Y_FWD_BLK && p->slab_p != 1) return fail(CTAP_EINVAL, "blocked k-space passes are single-GPU");
+  if (kind >= CTAP_PASS_Y_FWD_BLK && in == out && kind != CTAP_PASS_X_KIN_BLK)
+    return fail(CTAP_EINVAL, "blocked y passes run out of place");
   if (kind <= CTAP_PASS_Z_LAST && in != out) return fail(CTAP_EINVAL, "z passes run in place");
   if ((kind == CTAP_PASS_Z_FIRST || kind == CTAP_PASS_Z_MID || kind == CTAP_PASS_Z_LAST) && !p->vi_dev)
     return fail(CTAP_EINVAL, "plan has no potential");
@@ -148,9 +165,15 @@ CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Z_FIRST, psi, psi, st), "ctap_advance");
   for (int64_t j = 0; j < n; ++j) {
-    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Y_FWD, psi, psi, st), "ctap_advance");
-    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, st), "ctap_advance");
-    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Y_INV, psi, psi, st), "ctap_advance");
+    if (p->kbuf) {
+      CUDA_TRY(ctap_run_pass(p, ctap::PASS_Y_FWD_BLK, psi, p->kbuf, st), "ctap_advance");
+      CUDA_TRY(ctap_run_pass(p, ctap::PASS_X_KIN_BLK, p->kbuf, p->kbuf, st), "ctap_advance");
+      CUDA_TRY(ctap_run_pass(p, ctap::PASS_Y_INV_BLK, p->kbuf, psi, st), "ctap_advance");
+    } else {
+      CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Y_FWD, psi, psi, st), "ctap_advance");
+      CUDA_TRY(ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, st), "ctap_advance");
+      CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Y_INV, psi, psi, st), "ctap_advance");
+    }
     CUDA_TRY(ctap_run_pass(p, j < n - 1 ? CTAP_PASS_Z_MID : CTAP_PASS_Z_LAST, psi, psi, st), "ctap_advance");
   }
   return CTAP_OK;

@@ -101,9 +101,9 @@ struct Dft<8, DIR> {
 
 // Compile-time radix plan for a line of length L (8 <= L <= 1024): stages of
 // radix 8 followed by at most one radix-2 or radix-4 stage.
-template <int L>
+template <int L, int E = kElems>
 struct Plan {
-  static constexpr int T = L / kElems;  // threads per line
+  static constexpr int T = L / E;  // threads per line
   static constexpr int log2L = (L >= 1024) ? 10 : (L >= 512) ? 9 : (L >= 256) ? 8 : (L >= 128) ? 7
                                : (L >= 64) ? 6 : (L >= 32) ? 5 : (L >= 16) ? 4 : 3;
   static constexpr int n8 = log2L / 3;
@@ -161,10 +161,10 @@ struct SyncNamed {  // T threads (a multiple of 32) of one line: named barrier
 //   radix R, stride Ns (product of earlier radices), line length L.
 // Input: v[m] = x[t + m*T].  Output scattered to smem (unless last stage, in
 // which case v[m] = X[t + m*T] stays in registers).
-template <int L, int R, int NS, int TWO, int DIR, bool LAST, typename Smem>
+template <int L, int E, int R, int NS, int TWO, int DIR, bool LAST, typename Smem>
 __device__ __forceinline__ void stockham_stage(double2* v, int t, const double2* __restrict__ tw, Smem sm) {
-  constexpr int T = L / kElems;
-  constexpr int NB = kElems / R;  // butterflies per thread
+  constexpr int T = L / E;
+  constexpr int NB = E / R;  // butterflies per thread
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     double2 u[R];
@@ -192,32 +192,34 @@ __device__ __forceinline__ void stockham_stage(double2* v, int t, const double2*
   }
 }
 
-template <int L, int S, int DIR, typename Smem, typename Sync>
+template <int L, int E, int S, int DIR, typename Smem, typename Sync>
 __device__ __forceinline__ void fft_stages(double2* v, int t, const double2* __restrict__ tw, Smem sm,
                                            Sync sync) {
-  using P = Plan<L>;
+  using P = Plan<L, E>;
   constexpr int T = P::T;
   if constexpr (S < P::nstages) {
     constexpr int R = P::radix(S);
     constexpr int NS = P::ns(S);
     constexpr bool LAST = (S == P::nstages - 1);
-    stockham_stage<L, R, NS, P::tw_offset(S), DIR, LAST>(v, t, tw, sm);
+    stockham_stage<L, E, R, NS, P::tw_offset(S), DIR, LAST>(v, t, tw, sm);
     if constexpr (!LAST) {
       sync();
 #pragma unroll
-      for (int m = 0; m < kElems; ++m) v[m] = sm.at(t + m * T);
+      for (int m = 0; m < E; ++m) v[m] = sm.at(t + m * T);
       sync();
-      fft_stages<L, S + 1, DIR>(v, t, tw, sm, sync);
+      fft_stages<L, E, S + 1, DIR>(v, t, tw, sm, sync);
     }
   }
 }
 
 // Full in-register/shared 1D FFT of the thread's line.  On entry v[m] holds
-// x[t + m*T], on exit X[t + m*T] (unnormalized, sign DIR).  Every thread that
-// shares the exchange buffer must call it (barriers inside).
-template <int L, int DIR, typename Smem, typename Sync>
+// x[t + m*T], on exit X[t + m*T] (unnormalized, sign DIR), T = L/E threads
+// per line.  Every thread that shares the exchange buffer must call it
+// (barriers inside).  The radix plan (and hence the twiddle table) depends
+// only on L, not on E.
+template <int L, int DIR, int E = kElems, typename Smem, typename Sync>
 __device__ __forceinline__ void line_fft(double2* v, int t, const double2* __restrict__ tw, Smem sm, Sync sync) {
-  fft_stages<L, 0, DIR>(v, t, tw, sm, sync);
+  fft_stages<L, E, 0, DIR>(v, t, tw, sm, sync);
 }
 
 // --- exact phase recipes (reference propagator.py:61-68, qgrid.py:98-117) ---

@@ -23,6 +23,10 @@ enum PassKind {
   PASS_X_KIN = CTAP_PASS_X_KIN,  // Fx, K / N, Fx^-1
   PASS_X_FWD = CTAP_PASS_X_FWD,
   PASS_X_INV = CTAP_PASS_X_INV,
+  // blocked k-space variants of the single-GPU step (internal)
+  PASS_Y_FWD_BLK = CTAP_PASS_Y_FWD_BLK,  // y FFT, natural -> blocked k-space buffer
+  PASS_X_KIN_BLK = CTAP_PASS_X_KIN_BLK,  // [x K x^-1] on the blocked buffer, in place
+  PASS_Y_INV_BLK = CTAP_PASS_Y_INV_BLK,  // y^-1, blocked buffer -> natural
   // strided kernel variants
   PASS_S_FWD = 100,
   PASS_S_INV = 101,
@@ -44,6 +48,8 @@ struct ctap_plan {
   double* k2_dev[3];       // squared wavenumbers per axis (global lengths)
   double2* twiddles;       // stage-major twiddle tables for L = 8..1024
   int tw_off[8];           // start of the table of L = 8 << i
+  double2* kbuf;           // single-GPU k-space buffer (blocked layout, out of place y passes)
+  int k_lx;                // log2 of the x block of the k-space layout (0: natural)
   double* red_partial;     // reduction scratch
   int red_blocks;
 };

@@ -176,29 +176,44 @@ __global__ void __launch_bounds__(ZCfg<L>::threads, ZMinBlocks<KIND, VTAB>::valu
 // y and x passes
 // ---------------------------------------------------------------------------
 
+// points per thread of the strided kernels (8 or 16): 16 halves the threads
+// (and the barrier fan-in) per tile and doubles each thread's ILP
+#ifndef CTAP_TILE_E
+#define CTAP_TILE_E 8
+#endif
+
 template <int L>
 struct TileCfg {
-  static constexpr int T = L / kElems;
+  static constexpr int E = (L >= 256) ? CTAP_TILE_E : kElems;
+  static constexpr int T = L / E;
   static constexpr int per_tile = T * 8;
   static constexpr int G = per_tile >= 128 ? 1 : 128 / per_tile;  // tiles per block
   static constexpr int threads = G * per_tile;
   static constexpr size_t smem = (size_t)G * L * 8 * sizeof(double2);
-  static constexpr int minb = CTAP_OCC / threads > 0 ? CTAP_OCC / threads : 1;
+  static constexpr int occ = CTAP_OCC * kElems / E;  // same register file, E/8 x the registers
+  static constexpr int minb = occ / threads > 0 ? occ / threads : 1;
   static constexpr int minb_tab = CTAP_OCC_TAB / threads > 0 ? CTAP_OCC_TAB / threads : 1;
 };
 
-// Element (o, i, z) lives at
-//   natural:  o*so + i*si + z
-//   peer:     o*so + (i >> lb)*sb + (i & (2^lb - 1))*si + z   (slab transpose buffers)
+// Element (o, i, z) of a strided tile lives at outer(o) + inner(i) + z:
+//   outer(o) = (o >> olb)*osb + (o & (2^olb - 1))*so      (olb = 31: o*so)
+//   inner(i) = i*si                                       (plain)
+//            = (i >> lb)*sb + (i & (2^lb - 1))*si          (blocked: the slab
+//              transpose buffers and the blocked k-space layout)
 struct Layout {
   uint32_t so, sb, si;
   int lb;
+  uint32_t osb;
+  int olb;
 };
 
-template <bool PEER>
-__device__ __forceinline__ uint32_t lay(const Layout& l, uint32_t o, uint32_t i) {
-  if constexpr (PEER) return o * l.so + (i >> l.lb) * l.sb + (i & ((1u << l.lb) - 1u)) * l.si;
-  else return o * l.so + i * l.si;
+__device__ __forceinline__ uint32_t outer(const Layout& l, uint32_t o) {
+  return (o >> l.olb) * l.osb + (o & ((1u << l.olb) - 1u)) * l.so;
+}
+template <bool BLK>
+__device__ __forceinline__ uint32_t inner(const Layout& l, uint32_t i) {
+  if constexpr (BLK) return (i >> l.lb) * l.sb + (i & ((1u << l.lb) - 1u)) * l.si;
+  else return i * l.si;
 }
 
 struct TileArgs {
@@ -210,33 +225,41 @@ struct TileArgs {
   PhaseArgs ph;
 };
 
-template <int L, int KIND, bool KTAB>
+template <int L, int E, int KIND, bool KTAB, bool KBLK>
 __device__ __forceinline__ void tile_body(const TileArgs& a, double2* v, int t, uint32_t o, uint32_t z,
                                           bool active, const double2* __restrict__ tw, SmemStrided sm) {
-  constexpr int T = L / kElems;
+  constexpr int T = L / E;
   if constexpr (KIND == T_FWD) {
-    line_fft<L, -1>(v, t, tw, sm, SyncBlock{});
+    line_fft<L, -1, E>(v, t, tw, sm, SyncBlock{});
   } else if constexpr (KIND == T_INV) {
-    line_fft<L, +1>(v, t, tw, sm, SyncBlock{});
+    line_fft<L, +1, E>(v, t, tw, sm, SyncBlock{});
   } else {  // T_KIN: forward, K/N, inverse
-    double kx2[kElems], ky2 = 0.0, kz2 = 0.0;
-    if constexpr (!KTAB) {  // operands of the phase, loaded ahead of the forward transform
+    // operands of the phase, loaded ahead of the forward transform so their
+    // latency hides behind it
+    double kx2[E], ky2 = 0.0, kz2 = 0.0;
+    double2 f[E];
+    if constexpr (KTAB) {
+#pragma unroll
+      for (int m = 0; m < E; ++m)
+        f[m] = active ? __ldcg(&a.ph.expk[outer(a.lout, o) + inner<KBLK>(a.lout, t + m * T) + z])
+                      : make_double2(0.0, 0.0);
+    } else {
       ky2 = __ldg(&a.ph.ky2[a.ph.outer_off + o]);
       kz2 = __ldg(&a.ph.kz2[z]);
 #pragma unroll
-      for (int m = 0; m < kElems; ++m) kx2[m] = __ldg(&a.ph.kx2[t + m * T]);
+      for (int m = 0; m < E; ++m) kx2[m] = __ldg(&a.ph.kx2[t + m * T]);
     }
-    line_fft<L, -1>(v, t, tw, sm, SyncBlock{});
+    line_fft<L, -1, E>(v, t, tw, sm, SyncBlock{});
     if (active) {
       if constexpr (KTAB) {
 #pragma unroll
-        for (int m = 0; m < kElems; ++m) v[m] = cmul(v[m], __ldcg(&a.ph.expk[lay<false>(a.lout, o, t + m * T) + z]));
+        for (int m = 0; m < E; ++m) v[m] = cmul(v[m], f[m]);
       } else {
 #pragma unroll
-        for (int m = 0; m < kElems; ++m) mul_kphase(v[m], kx2[m], ky2, kz2, a.ph);
+        for (int m = 0; m < E; ++m) mul_kphase(v[m], kx2[m], ky2, kz2, a.ph);
       }
     }
-    line_fft<L, +1>(v, t, tw, sm, SyncBlock{});
+    line_fft<L, +1, E>(v, t, tw, sm, SyncBlock{});
   }
 }
 
@@ -252,14 +275,15 @@ __global__ void __launch_bounds__(TileCfg<L>::threads, KTAB ? TileCfg<L>::minb_t
   const bool active = tile < a.n_outer * a.nchunk;
   const uint32_t o = active ? tile / a.nchunk : 0;
   const uint32_t z = (active ? (tile - o * a.nchunk) : 0) * 8 + col;
-  double2 v[kElems];
+  constexpr int E = C::E;
+  const uint32_t obi = outer(a.lin, o) + z, obo = outer(a.lout, o) + z;
+  double2 v[E];
 #pragma unroll
-  for (int m = 0; m < kElems; ++m)
-    v[m] = active ? a.in[lay<PIN>(a.lin, o, t + m * C::T) + z] : make_double2(0.0, 0.0);
-  tile_body<L, KIND, KTAB>(a, v, t, o, z, active, tw, SmemStrided{smem + (size_t)g * L * 8 + col});
+  for (int m = 0; m < E; ++m) v[m] = active ? a.in[obi + inner<PIN>(a.lin, t + m * C::T)] : make_double2(0.0, 0.0);
+  tile_body<L, E, KIND, KTAB, POUT>(a, v, t, o, z, active, tw, SmemStrided{smem + (size_t)g * L * 8 + col});
   if (active) {
 #pragma unroll
-    for (int m = 0; m < kElems; ++m) a.out[lay<POUT>(a.lout, o, t + m * C::T) + z] = v[m];
+    for (int m = 0; m < E; ++m) a.out[obo + inner<POUT>(a.lout, t + m * C::T)] = v[m];
   }
 }
 
@@ -333,22 +357,25 @@ __global__ void phase_field_kernel(double2* __restrict__ out, const double* __re
                                    const double* __restrict__ kx2, const double* __restrict__ ky2,
                                    const double* __restrict__ kz2, uint32_t nx, uint32_t ny, uint32_t nz,
                                    uint32_t x_off, uint32_t y_off, int which, int imag, double dt_i,
-                                   double len2, double scale) {
+                                   double len2, double scale, int lx) {
   const uint32_t n = nx * ny * nz;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double phi;
+    uint32_t dst = i;
     if (which == 2) {
       const uint32_t x = i / (ny * nz), y = (i / nz) % ny, z = i % nz;
       phi = k_phase(kx2[x + x_off], ky2[y + y_off], kz2[z], len2, dt_i);
+      // blocked k-space position (lx = 0: natural)
+      dst = (((x >> lx) * ny + y) << lx) * nz + (x & ((1u << lx) - 1u)) * nz + z;
     } else {
       phi = v_phase_i(vi[i], which == 0 ? -0.5 : -1.0, dt_i);
     }
     if (imag) {
-      out[i] = make_double2(exp(phi) * scale, 0.0);
+      out[dst] = make_double2(exp(phi) * scale, 0.0);
     } else {
       double s, c;
       fast_sincos(phi, &s, &c);
-      out[i] = make_double2(c * scale, s * scale);
+      out[dst] = make_double2(c * scale, s * scale);
     }
   }
 }
@@ -408,12 +435,12 @@ cudaError_t ctap_run_phase_field(const ctap_plan* p, int which, void* out, cudaS
     const uint32_t nyl = (uint32_t)(p->n[1] / p->slab_p);
     phase_field_kernel<<<p->red_blocks, 256, 0, st>>>(
         (double2*)out, p->vi_dev, p->k2_dev[0], p->k2_dev[1], p->k2_dev[2], (uint32_t)p->n[0], nyl,
-        (uint32_t)p->n[2], 0u, (uint32_t)p->slab_r * nyl, 2, imag, p->dt_i, p->len2, p->inv_scale);
+        (uint32_t)p->n[2], 0u, (uint32_t)p->slab_r * nyl, 2, imag, p->dt_i, p->len2, p->inv_scale, p->k_lx);
   } else {
     phase_field_kernel<<<p->red_blocks, 256, 0, st>>>(
         (double2*)out, p->vi_dev, p->k2_dev[0], p->k2_dev[1], p->k2_dev[2], (uint32_t)p->nx_local,
         (uint32_t)p->n[1], (uint32_t)p->n[2], (uint32_t)(p->slab_r * p->nx_local), 0u, which, imag, p->dt_i,
-        p->len2, 1.0);
+        p->len2, 1.0, 0);
   }
   return cudaGetLastError();
 }
@@ -460,12 +487,44 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
   a.out = (double2*)out;
   a.nchunk = (uint32_t)(nz / 8);
   a.ph = ph;
-  // natural x-slab layout (x_local, y, z), lines along y
-  const Layout y_nat{(uint32_t)(ny * nz), 0u, (uint32_t)nz, 0};
-  // peer-major layout [peer][x_local][y_local][z] for the y <-> x transposes
-  const Layout y_peer{nyl * (uint32_t)nz, nxl * nyl * (uint32_t)nz, (uint32_t)nz, ilog2(nyl)};
+  const uint32_t NZ = (uint32_t)nz, NY = (uint32_t)ny;
+  constexpr int kNone = 31;  // no outer blocking
+  // natural x-slab layout (x_local, y, z), y-pass view (o = x_local, i = y)
+  const Layout y_nat{NY * NZ, 0u, NZ, 0, 0u, kNone};
+  // peer-major [peer][x_local][y_local][z] (slab transpose buffers)
+  const Layout y_peer{nyl * NZ, nxl * nyl * NZ, NZ, ilog2(nyl), 0u, kNone};
+  // natural y-slab layout (x, y_local, z), x-pass view (o = y_local, i = x)
+  const Layout x_nat{NZ, 0u, nyl * NZ, 0, 0u, kNone};
+  // blocked k-space layout of the single-GPU step, B(x, y, z) =
+  //   ((x >> lx) ny + y) XL nz + (x & (XL-1)) nz + z,  XL = 2^lx:
+  // x-lines then span nx/XL TLB pages instead of nx
+  const int lx = p->k_lx;
+  const uint32_t XL = 1u << lx;
+  const Layout y_blk{NZ, 0u, XL * NZ, 0, NY * XL * NZ, lx};    // y-pass view
+  const Layout x_blk{XL * NZ, NY * XL * NZ, NZ, lx, 0u, kNone};  // x-pass view
   const bool peer = P > 1;
   switch (kind) {
+    case PASS_Y_FWD_BLK:
+    case PASS_Y_INV_BLK: {
+      a.n_outer = nxl;
+      const double2* tw = p->twiddles + p->tw_off[ilog2(ny) - 3];
+      if (kind == PASS_Y_FWD_BLK) {
+        a.lin = y_nat;
+        a.lout = y_blk;
+        return dispatch_tile<T_FWD, false, false, false>((int)ny, a, tw, st);
+      }
+      a.lin = y_blk;
+      a.lout = y_nat;
+      return dispatch_tile<T_INV, false, false, false>((int)ny, a, tw, st);
+    }
+    case PASS_X_KIN_BLK: {
+      a.lin = x_blk;
+      a.lout = x_blk;
+      a.n_outer = NY;
+      const double2* tw = p->twiddles + p->tw_off[ilog2(nx) - 3];
+      return p->expk_dev ? dispatch_tile<T_KIN, true, true, true>((int)nx, a, tw, st)
+                         : dispatch_tile<T_KIN, true, true, false>((int)nx, a, tw, st);
+    }
     case PASS_Y_FWD:
     case PASS_Y_INV:
     case PASS_Y_FWD_TO_PEER:
@@ -492,8 +551,6 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
     case PASS_X_KIN:
     case PASS_X_FWD:
     case PASS_X_INV: {
-      // y-slab layout (x, y_local, z): lines along x, outer index = local y
-      const Layout x_nat{(uint32_t)nz, 0u, nyl * (uint32_t)nz, 0};
       a.lin = x_nat;
       a.lout = x_nat;
       a.n_outer = nyl;
@@ -501,8 +558,8 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       const double2* tw = p->twiddles + p->tw_off[ilog2(nx) - 3];
       const int L = (int)nx;
       if (kind == PASS_X_KIN)
-        return p->expk_dev ? dispatch_tile<T_KIN, false, false, true>(L, a, tw, st)
-                           : dispatch_tile<T_KIN, false, false, false>(L, a, tw, st);
+        return p->expk_dev && p->k_lx == 0 ? dispatch_tile<T_KIN, false, false, true>(L, a, tw, st)
+                                           : dispatch_tile<T_KIN, false, false, false>(L, a, tw, st);
       if (kind == PASS_X_FWD) return dispatch_tile<T_FWD, false, false, false>(L, a, tw, st);
       return dispatch_tile<T_INV, false, false, false>(L, a, tw, st);
     }

@@ -29,16 +29,21 @@ def main():
     P = _lib
     passes = [("Z_MID", P.PASS_Z_MID, 40), ("Y_FWD", P.PASS_Y_FWD, 32), ("X_KIN", P.PASS_X_KIN, 32),
               ("Y_INV", P.PASS_Y_INV, 32), ("Z_FIRST", P.PASS_Z_FIRST, 40), ("Z_LAST", P.PASS_Z_LAST, 40),
-              ("Z_FWD", P.PASS_Z_FWD, 32)]
+              ("Z_FWD", P.PASS_Z_FWD, 32), ("X_FWD", P.PASS_X_FWD, 32), ("X_INV", P.PASS_X_INV, 32)]
+    kbuf = torch.empty_like(psi)
+    passes += [("Y_FWD_BLK", P.PASS_Y_FWD_BLK, 32), ("X_KIN_BLK", P.PASS_X_KIN_BLK, 32),
+               ("Y_INV_BLK", P.PASS_Y_INV_BLK, 32)]
+    io = {P.PASS_Y_FWD_BLK: (psi, kbuf), P.PASS_X_KIN_BLK: (kbuf, kbuf), P.PASS_Y_INV_BLK: (kbuf, psi)}
     total = 0.0
     for name, kind, bpp in passes:
+        src, dst = io.get(kind, (psi, psi))
         for _ in range(3):
-            plan.native.run_pass(kind, psi, psi)
+            plan.native.run_pass(kind, src, dst)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         s.record()
         for _ in range(reps):
-            plan.native.run_pass(kind, psi, psi)
+            plan.native.run_pass(kind, src, dst)
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / reps
