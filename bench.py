@@ -239,9 +239,36 @@ def run_ours(args):
     except Exception:
         pass
 
-    # end to end through the public API (single GPU): host-resident psi in
-    # pinned memory -> evolve_real with a population observer -> psi back on host
+    # end to end through the public API: host-resident psi in pinned memory ->
+    # evolve_real with a population observer (single GPU) or the slab
+    # propagator with the same event schedule (N GPUs) -> psi back on the host
     e2e = None
+    if world > 1 and not args.no_e2e:
+        host = torch.empty(lay.slab_shape, dtype=torch.complex128, pin_memory=True)
+        host.copy_(amp0)
+        host_out = torch.empty_like(host).pin_memory()
+        part = observables.symmetric_partition(grid, 3.5e-6)
+        stride = max(1, args.steps // 4)
+        events = propagator.event_schedule(args.steps, [observables.PopulationRecorder(part, stride=stride)])
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d = host.to(dev, non_blocking=True)
+        cur, rows = 0, []
+        for ev in events:
+            if ev > cur:
+                prop.advance(d, ev - cur)
+                cur = ev
+            rows.append(prop.observe(d, part.xb1, part.xb2, 2))
+        host_out.copy_(d)
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": args.steps / t_e2e, "unit": "steps/s",
+               "h2d_bytes_per_step": 16 * npts / args.steps,
+               "d2h_bytes_per_step": (16 * npts + len(rows) * 5 * 8 * world) / args.steps,
+               "path": "slab.SlabPropagator.advance/observe on host-resident slabs (pinned), max over ranks",
+               "observer_events": len(rows), "seconds": t_e2e}
+        del host, host_out, d
     if world == 1 and not args.no_e2e:
         host = torch.empty(grid.n, dtype=torch.complex128, pin_memory=True)
         host.copy_(amp0)

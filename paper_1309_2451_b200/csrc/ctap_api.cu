@@ -145,7 +145,9 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
 
 CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, void* stream) {
   if (!p || !in || !out) return fail(CTAP_EINVAL, "null argument");
-  if (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_Y_INV_BLK) return fail(CTAP_EINVAL, "unknown pass %d", kind);
+  const bool diag = kind == ctap::PASS_Y_COPY || kind == ctap::PASS_X_COPY;
+  if (!diag && (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_Y_INV_BLK))
+    return fail(CTAP_EINVAL, "unknown pass %d", kind);
   if (kind >= CTAP_PASS_Y_FWD_BLK && p->slab_p != 1) return fail(CTAP_EINVAL, "blocked k-space passes are single-GPU");
   if (kind >= CTAP_PASS_Y_FWD_BLK && in == out && kind != CTAP_PASS_X_KIN_BLK)
     return fail(CTAP_EINVAL, "blocked y passes run out of place");

@@ -27,6 +27,9 @@ enum PassKind {
   PASS_Y_FWD_BLK = CTAP_PASS_Y_FWD_BLK,  // y FFT, natural -> blocked k-space buffer
   PASS_X_KIN_BLK = CTAP_PASS_X_KIN_BLK,  // [x K x^-1] on the blocked buffer, in place
   PASS_Y_INV_BLK = CTAP_PASS_Y_INV_BLK,  // y^-1, blocked buffer -> natural
+  // diagnostics: the strided passes' memory traffic without the transforms
+  PASS_Y_COPY = 60,
+  PASS_X_COPY = 61,
   // strided kernel variants
   PASS_S_FWD = 100,
   PASS_S_INV = 101,

@@ -46,7 +46,7 @@
 
 namespace ctap {
 
-enum TileKind { T_FWD, T_INV, T_KIN, T_VFIRST, T_VMID, T_VLAST };
+enum TileKind { T_FWD, T_INV, T_KIN, T_VFIRST, T_VMID, T_VLAST, T_COPY };
 
 struct PhaseArgs {
   const double* vi;     // v_i = (V - shift)/E0 at the element offsets of psi (z passes)
@@ -229,7 +229,8 @@ template <int L, int E, int KIND, bool KTAB, bool KBLK>
 __device__ __forceinline__ void tile_body(const TileArgs& a, double2* v, int t, uint32_t o, uint32_t z,
                                           bool active, const double2* __restrict__ tw, SmemStrided sm) {
   constexpr int T = L / E;
-  if constexpr (KIND == T_FWD) {
+  if constexpr (KIND == T_COPY) {  // diagnostics: the pass's memory traffic without the transform
+  } else if constexpr (KIND == T_FWD) {
     line_fft<L, -1, E>(v, t, tw, sm, SyncBlock{});
   } else if constexpr (KIND == T_INV) {
     line_fft<L, +1, E>(v, t, tw, sm, SyncBlock{});
@@ -548,6 +549,16 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       return fwd ? dispatch_tile<T_FWD, false, false, false>(L, a, tw, st)
                  : dispatch_tile<T_INV, false, false, false>(L, a, tw, st);
     }
+    case PASS_Y_COPY:
+      a.n_outer = nxl;
+      a.lin = y_nat;
+      a.lout = y_nat;
+      return dispatch_tile<T_COPY, false, false, false>((int)ny, a, p->twiddles, st);
+    case PASS_X_COPY:
+      a.n_outer = nyl;
+      a.lin = x_nat;
+      a.lout = x_nat;
+      return dispatch_tile<T_COPY, false, false, false>((int)nx, a, p->twiddles, st);
     case PASS_X_KIN:
     case PASS_X_FWD:
     case PASS_X_INV: {
