@@ -41,6 +41,12 @@ typedef enum ctap_status {
   CTAP_ENOMEM = 4
 } ctap_status;
 
+typedef enum ctap_dtype {
+  CTAP_C128 = 0,  /* complex128 wavefunction (the reference's dtype) */
+  CTAP_C64 = 1    /* optional complex64 mode: complex64 storage and transforms,
+                     phases still evaluated exactly in FP64 (gate <= 1e-4) */
+} ctap_dtype;
+
 typedef enum ctap_mode {
   CTAP_REAL_TIME = 0,      /* propagator.REAL_TIME */
   CTAP_IMAGINARY_TIME = 1  /* propagator.IMAGINARY_TIME */
@@ -90,6 +96,8 @@ typedef struct ctap_plan_desc {
                            clear bit recomputes that factor per point every
                            step.  All variants use the identical phase
                            arithmetic (real time only; ignored otherwise). */
+  int32_t dtype;    /* ctap_dtype of every wavefunction buffer passed to the plan */
+  int32_t reserved;
 } ctap_plan_desc;
 
 /* make_plan (propagator.py:55-81).  kx2/ky2/kz2 are HOST arrays of the squared

@@ -22,6 +22,9 @@ CTAP_EUNSUPPORTED = 3
 REAL_TIME_MODE = 0
 IMAGINARY_TIME_MODE = 1
 
+DTYPE_C128 = 0
+DTYPE_C64 = 1
+
 # ctap_pass_kind
 PASS_Z_FWD, PASS_Z_INV, PASS_Z_FIRST, PASS_Z_MID, PASS_Z_LAST = range(5)
 PASS_Y_FWD, PASS_Y_INV, PASS_Y_FWD_TO_PEER, PASS_Y_INV_FROM_PEER = range(5, 9)
@@ -47,6 +50,8 @@ class CtapPlanDesc(ctypes.Structure):
         ("slab_p", ctypes.c_int32),
         ("slab_r", ctypes.c_int32),
         ("phase_tables", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -64,6 +64,7 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
                   (long long)d->n[i]);
   if (d->mode != CTAP_REAL_TIME && d->mode != CTAP_IMAGINARY_TIME)
     return fail(CTAP_EINVAL, "unknown mode %d", d->mode);
+  if (d->dtype != CTAP_C128 && d->dtype != CTAP_C64) return fail(CTAP_EINVAL, "unknown dtype %d", d->dtype);
   int P = d->slab_p < 1 ? 1 : d->slab_p;
   if (d->n[0] % P || d->n[1] % P) return fail(CTAP_EINVAL, "nx and ny must be divisible by the %d slab ranks", P);
   if (d->slab_r < 0 || d->slab_r >= P) return fail(CTAP_EINVAL, "slab rank %d out of range", d->slab_r);
@@ -75,6 +76,7 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   p->slab_r = d->slab_r;
   p->nx_local = d->n[0] / P;
   p->mode = d->mode;
+  p->dtype = d->dtype;
   p->e0 = d->e0;
   p->dt_i = d->dt_i;
   p->len2 = d->len2;
@@ -91,12 +93,18 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   std::vector<double> tw = ctap_make_twiddles(p->tw_off);
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->twiddles, tw.size() * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(p->twiddles, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {  // complex64 copy of the (correctly rounded) double table
+    std::vector<float> tw32(tw.begin(), tw.end());
+    e = cudaMalloc((void**)&p->twiddles32, tw32.size() * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(p->twiddles32, tw32.data(), tw32.size() * sizeof(float), cudaMemcpyHostToDevice);
+  }
   int dev = 0, sms = 148;
   if (e == cudaSuccess) e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   p->red_blocks = sms * 4;
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->red_partial, sizeof(double) * 8 * p->red_blocks);
   const size_t nloc = (size_t)p->nx_local * d->n[1] * d->n[2];
+  const size_t csize = p->dtype == CTAP_C64 ? sizeof(float2) : sizeof(double2);
   // single GPU, opt-in (CTAP_KBLK_LX=lx > 0): out-of-place y passes into a
   // blocked k-space buffer so an x-line spans nx/2^lx address blocks instead of
   // nx.  Measured slower than the in-place natural layout on B200 at 512^3
@@ -107,19 +115,19 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
     if (const char* env = getenv("CTAP_KBLK_LX")) lx = atoi(env);
     while (lx > 0 && (int64_t(1) << lx) > d->n[0]) --lx;
     p->k_lx = lx < 0 ? 0 : lx;
-    if (p->k_lx > 0 && e == cudaSuccess) e = cudaMalloc((void**)&p->kbuf, sizeof(double2) * nloc);
+    if (p->k_lx > 0 && e == cudaSuccess) e = cudaMalloc((void**)&p->kbuf, csize * nloc);
   }
   if (v_dev) {  // a plan without a potential only serves FFTs and reductions
     if (e == cudaSuccess) e = cudaMalloc((void**)&p->vi_dev, sizeof(double) * nloc);
     if (e == cudaSuccess) e = ctap_run_v_internal(p, 0);
   }
   if (e == cudaSuccess && v_dev && (d->phase_tables & 1) && d->mode == CTAP_REAL_TIME) {
-    e = cudaMalloc((void**)&p->expv_dev, sizeof(double2) * nloc);
-    if (e == cudaSuccess) e = ctap_run_phase_field(p, 1, p->expv_dev, 0);
+    e = cudaMalloc((void**)&p->expv_dev, csize * nloc);
+    if (e == cudaSuccess) e = ctap_run_phase_table(p, 1, p->expv_dev, 0);
   }
   if (e == cudaSuccess && (d->phase_tables & 2) && d->mode == CTAP_REAL_TIME) {
-    e = cudaMalloc((void**)&p->expk_dev, sizeof(double2) * nloc);
-    if (e == cudaSuccess) e = ctap_run_phase_field(p, 3, p->expk_dev, 0);
+    e = cudaMalloc((void**)&p->expk_dev, csize * nloc);
+    if (e == cudaSuccess) e = ctap_run_phase_table(p, 3, p->expk_dev, 0);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -134,6 +142,7 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
   if (!p) return CTAP_OK;
   for (int i = 0; i < 3; ++i) cudaFree(p->k2_dev[i]);
   cudaFree(p->twiddles);
+  cudaFree(p->twiddles32);
   cudaFree(p->red_partial);
   cudaFree(p->vi_dev);
   cudaFree(p->expv_dev);
@@ -148,9 +157,9 @@ CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, vo
   const bool diag = kind == ctap::PASS_Y_COPY || kind == ctap::PASS_X_COPY;
   if (!diag && (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_Y_INV_BLK))
     return fail(CTAP_EINVAL, "unknown pass %d", kind);
-  if (kind >= CTAP_PASS_Y_FWD_BLK && p->slab_p != 1) return fail(CTAP_EINVAL, "blocked k-space passes are single-GPU");
-  if (kind >= CTAP_PASS_Y_FWD_BLK && in == out && kind != CTAP_PASS_X_KIN_BLK)
-    return fail(CTAP_EINVAL, "blocked y passes run out of place");
+  const bool blk = kind >= CTAP_PASS_Y_FWD_BLK && kind <= CTAP_PASS_Y_INV_BLK;
+  if (blk && p->slab_p != 1) return fail(CTAP_EINVAL, "blocked k-space passes are single-GPU");
+  if (blk && in == out && kind != CTAP_PASS_X_KIN_BLK) return fail(CTAP_EINVAL, "blocked y passes run out of place");
   if (kind <= CTAP_PASS_Z_LAST && in != out) return fail(CTAP_EINVAL, "z passes run in place");
   if ((kind == CTAP_PASS_Z_FIRST || kind == CTAP_PASS_Z_MID || kind == CTAP_PASS_Z_LAST) && !p->vi_dev)
     return fail(CTAP_EINVAL, "plan has no potential");

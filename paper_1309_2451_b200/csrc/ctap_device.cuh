@@ -24,22 +24,46 @@ namespace ctap {
 
 constexpr int kElems = 8;  // points per thread per line
 
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// Complex vector types: double2 (complex128, the reference's dtype) and
+// float2 (the optional complex64 mode).  CT<C> maps a vector type to its
+// scalar and builder.
+template <typename C>
+struct CT;
+template <>
+struct CT<double2> {
+  using R = double;
+  __device__ __forceinline__ static double2 mk(double a, double b) { return make_double2(a, b); }
+};
+template <>
+struct CT<float2> {
+  using R = float;
+  __device__ __forceinline__ static float2 mk(float a, float b) { return make_float2(a, b); }
+};
+
+template <typename C>
+__device__ __forceinline__ C cadd(C a, C b) { return CT<C>::mk(a.x + b.x, a.y + b.y); }
+template <typename C>
+__device__ __forceinline__ C csub(C a, C b) { return CT<C>::mk(a.x - b.x, a.y - b.y); }
 // complex products with an explicit FMA pattern, so the rounding does not
 // depend on how the compiler contracts the surrounding code (keeps e.g. the
 // slab and single-GPU paths bitwise identical)
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -__dmul_rn(a.y, b.y)), fma(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -__fmul_rn(a.y, b.y)), fmaf(a.x, b.y, __fmul_rn(a.y, b.x)));
+}
 // a * conj(b)
 __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, __dmul_rn(a.y, b.y)), fma(a.y, b.x, -__dmul_rn(a.x, b.y)));
 }
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, __fmul_rn(a.y, b.y)), fmaf(a.y, b.x, -__fmul_rn(a.x, b.y)));
+}
 // multiply by -i (DIR=-1, forward) or +i (DIR=+1, inverse)
-template <int DIR>
-__device__ __forceinline__ double2 mul_i(double2 a) {
-  return DIR < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+template <int DIR, typename C>
+__device__ __forceinline__ C mul_i(C a) {
+  return DIR < 0 ? CT<C>::mk(a.y, -a.x) : CT<C>::mk(-a.y, a.x);
 }
 
 // In-register DFT of size R with sign DIR (-1 forward, +1 inverse),
@@ -49,8 +73,9 @@ struct Dft;
 
 template <int DIR>
 struct Dft<2, DIR> {
-  __device__ __forceinline__ static void run(double2* v) {
-    double2 a = v[0], b = v[1];
+  template <typename C>
+  __device__ __forceinline__ static void run(C* v) {
+    C a = v[0], b = v[1];
     v[0] = cadd(a, b);
     v[1] = csub(a, b);
   }
@@ -58,11 +83,12 @@ struct Dft<2, DIR> {
 
 template <int DIR>
 struct Dft<4, DIR> {
-  __device__ __forceinline__ static void run(double2* v) {
-    double2 t0 = cadd(v[0], v[2]);
-    double2 t1 = csub(v[0], v[2]);
-    double2 t2 = cadd(v[1], v[3]);
-    double2 t3 = mul_i<DIR>(csub(v[1], v[3]));
+  template <typename C>
+  __device__ __forceinline__ static void run(C* v) {
+    C t0 = cadd(v[0], v[2]);
+    C t1 = csub(v[0], v[2]);
+    C t2 = cadd(v[1], v[3]);
+    C t3 = mul_i<DIR>(csub(v[1], v[3]));
     v[0] = cadd(t0, t2);
     v[2] = csub(t0, t2);
     v[1] = cadd(t1, t3);
@@ -72,22 +98,24 @@ struct Dft<4, DIR> {
 
 template <int DIR>
 struct Dft<8, DIR> {
-  __device__ __forceinline__ static void run(double2* v) {
-    constexpr double h = 0.70710678118654752440;  // sqrt(2)/2
-    double2 e[4] = {v[0], v[2], v[4], v[6]};
-    double2 o[4] = {v[1], v[3], v[5], v[7]};
+  template <typename C>
+  __device__ __forceinline__ static void run(C* v) {
+    using R = typename CT<C>::R;
+    constexpr R h = (R)0.70710678118654752440;  // sqrt(2)/2
+    C e[4] = {v[0], v[2], v[4], v[6]};
+    C o[4] = {v[1], v[3], v[5], v[7]};
     Dft<4, DIR>::run(e);
     Dft<4, DIR>::run(o);
     // o[k] *= exp(DIR i pi k / 4)
-    double2 o1, o3;
+    C o1, o3;
     if (DIR < 0) {
-      o1 = make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-      o3 = make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+      o1 = CT<C>::mk(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
+      o3 = CT<C>::mk(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
     } else {
-      o1 = make_double2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y));
-      o3 = make_double2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y));
+      o1 = CT<C>::mk(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y));
+      o3 = CT<C>::mk(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y));
     }
-    double2 o2 = mul_i<DIR>(o[2]);
+    C o2 = mul_i<DIR>(o[2]);
     v[0] = cadd(e[0], o[0]);
     v[4] = csub(e[0], o[0]);
     v[1] = cadd(e[1], o1);
@@ -134,13 +162,15 @@ __device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
 
 // Accessor abstractions for the exchange buffer: element i of the thread's
 // line, where `base` already selects the line (contiguous) or column (strided).
+template <typename C>
 struct SmemContig {
-  double2* base;
-  __device__ __forceinline__ double2& at(int i) const { return base[pad8(i)]; }
+  C* base;
+  __device__ __forceinline__ C& at(int i) const { return base[pad8(i)]; }
 };
+template <typename C>
 struct SmemStrided {  // column-fastest tile: element i of column c at i*8 + c
-  double2* base;      // points at column c
-  __device__ __forceinline__ double2& at(int i) const { return base[i * 8]; }
+  C* base;            // points at column c
+  __device__ __forceinline__ C& at(int i) const { return base[i * 8]; }
 };
 
 // Barrier among the threads that share one exchange buffer.
@@ -161,13 +191,13 @@ struct SyncNamed {  // T threads (a multiple of 32) of one line: named barrier
 //   radix R, stride Ns (product of earlier radices), line length L.
 // Input: v[m] = x[t + m*T].  Output scattered to smem (unless last stage, in
 // which case v[m] = X[t + m*T] stays in registers).
-template <int L, int E, int R, int NS, int TWO, int DIR, bool LAST, typename Smem>
-__device__ __forceinline__ void stockham_stage(double2* v, int t, const double2* __restrict__ tw, Smem sm) {
+template <int L, int E, int R, int NS, int TWO, int DIR, bool LAST, typename C, typename Smem>
+__device__ __forceinline__ void stockham_stage(C* v, int t, const C* __restrict__ tw, Smem sm) {
   constexpr int T = L / E;
   constexpr int NB = E / R;  // butterflies per thread
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    double2 u[R];
+    C u[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) u[r] = v[b + r * NB];
     const int j = t + b * T;
@@ -176,7 +206,7 @@ __device__ __forceinline__ void stockham_stage(double2* v, int t, const double2*
       // twiddle exp(DIR 2 pi i r k / (NS R)) from the stage-major table
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        double2 w = __ldg(&tw[TWO + (r - 1) * NS + k]);
+        C w = __ldg(&tw[TWO + (r - 1) * NS + k]);
         u[r] = DIR < 0 ? cmul(u[r], w) : cmulc(u[r], w);
       }
     }
@@ -192,8 +222,8 @@ __device__ __forceinline__ void stockham_stage(double2* v, int t, const double2*
   }
 }
 
-template <int L, int E, int S, int DIR, typename Smem, typename Sync>
-__device__ __forceinline__ void fft_stages(double2* v, int t, const double2* __restrict__ tw, Smem sm,
+template <int L, int E, int S, int DIR, typename C, typename Smem, typename Sync>
+__device__ __forceinline__ void fft_stages(C* v, int t, const C* __restrict__ tw, Smem sm,
                                            Sync sync) {
   using P = Plan<L, E>;
   constexpr int T = P::T;
@@ -217,8 +247,8 @@ __device__ __forceinline__ void fft_stages(double2* v, int t, const double2* __r
 // per line.  Every thread that shares the exchange buffer must call it
 // (barriers inside).  The radix plan (and hence the twiddle table) depends
 // only on L, not on E.
-template <int L, int DIR, int E = kElems, typename Smem, typename Sync>
-__device__ __forceinline__ void line_fft(double2* v, int t, const double2* __restrict__ tw, Smem sm, Sync sync) {
+template <int L, int DIR, int E = kElems, typename C, typename Smem, typename Sync>
+__device__ __forceinline__ void line_fft(C* v, int t, const C* __restrict__ tw, Smem sm, Sync sync) {
   fft_stages<L, E, 0, DIR>(v, t, tw, sm, sync);
 }
 

@@ -46,10 +46,12 @@ struct ctap_plan {
   double inv_scale;        // 1 / (nx ny nz), exact power of two
   const double* v_dev;     // caller-owned potential slab (J)
   double* vi_dev;          // v_i = (V - v_shift) / e0, plan-owned (propagator.py:65, :75)
-  double2* expv_dev;       // optional table exp(-i v_i dt_i)       (phase_tables, real time)
-  double2* expk_dev;       // optional table exp(-i k^2 dt/2) / N, x-pass layout
+  void* expv_dev;          // optional table exp(-i v_i dt_i), plan precision (phase_tables, real time)
+  void* expk_dev;          // optional table exp(-i k^2 dt/2) / N, x-pass layout
   double* k2_dev[3];       // squared wavenumbers per axis (global lengths)
+  int dtype;               // CTAP_C128 or CTAP_C64
   double2* twiddles;       // stage-major twiddle tables for L = 8..1024
+  float2* twiddles32;      // the same, rounded to float (complex64 mode)
   int tw_off[8];           // start of the table of L = 8 << i
   double2* kbuf;           // single-GPU k-space buffer (blocked layout, out of place y passes)
   int k_lx;                // log2 of the x block of the k-space layout (0: natural)
@@ -59,6 +61,7 @@ struct ctap_plan {
 
 cudaError_t ctap_run_v_internal(const ctap_plan* p, cudaStream_t st);
 cudaError_t ctap_run_phase_field(const ctap_plan* p, int which, void* out, cudaStream_t st);
+cudaError_t ctap_run_phase_table(const ctap_plan* p, int which, void* out, cudaStream_t st);
 #include <vector>
 std::vector<double> ctap_make_twiddles(int off[8]);
 cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* out, cudaStream_t st);

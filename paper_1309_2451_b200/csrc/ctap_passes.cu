@@ -50,11 +50,11 @@ enum TileKind { T_FWD, T_INV, T_KIN, T_VFIRST, T_VMID, T_VLAST, T_COPY };
 
 struct PhaseArgs {
   const double* vi;     // v_i = (V - shift)/E0 at the element offsets of psi (z passes)
-  const double2* expv;  // exp(-i v_i dt_i) table (z passes, VTAB)
+  const void* expv;     // exp(-i v_i dt_i) table, complex of the plan's precision (VTAB)
   const double* kx2;    // k^2 along the pass axis (x pass)
   const double* ky2;    // k^2 along the outer axis, global
   const double* kz2;    // k^2 along z
-  const double2* expk;  // exp(-i k^2 dt/2)/N table in the x-pass layout (KTAB)
+  const void* expk;     // exp(-i k^2 dt/2)/N table in the x-pass layout (KTAB)
   uint32_t outer_off;   // global index of outer o = 0
   double len2, dt_i;
   double scale;         // folded inverse normalisation 1/N (power of two)
@@ -62,28 +62,34 @@ struct PhaseArgs {
 };
 
 // v *= exp(i coef v_i dt) (real time) or exp(coef v_i dt) (imaginary time)
-__device__ __forceinline__ void mul_vphase(double2& v, double vi, double coef, const PhaseArgs& a) {
+// (the phase and its cos/sin are always evaluated in FP64; complex64 mode
+// rounds the factor to float)
+template <typename CV>
+__device__ __forceinline__ void mul_vphase(CV& v, double vi, double coef, const PhaseArgs& a) {
+  using R = typename CT<CV>::R;
   const double phi = v_phase_i(vi, coef, a.dt_i);
   if (a.imag) {
-    const double f = exp(phi);
-    v = make_double2(v.x * f, v.y * f);
+    const R f = (R)exp(phi);
+    v = CT<CV>::mk(v.x * f, v.y * f);
   } else {
     double s, c;
     fast_sincos(phi, &s, &c);
-    v = cmul(v, make_double2(c, s));
+    v = cmul(v, CT<CV>::mk((R)c, (R)s));
   }
 }
 
 // v *= exp(-i k^2 dt/2) / N at (kx2, ky2, kz2)
-__device__ __forceinline__ void mul_kphase(double2& v, double kx2, double ky2, double kz2, const PhaseArgs& a) {
+template <typename CV>
+__device__ __forceinline__ void mul_kphase(CV& v, double kx2, double ky2, double kz2, const PhaseArgs& a) {
+  using R = typename CT<CV>::R;
   const double phi = k_phase(kx2, ky2, kz2, a.len2, a.dt_i);
   if (a.imag) {
-    const double f = exp(phi) * a.scale;
-    v = make_double2(v.x * f, v.y * f);
+    const R f = (R)(exp(phi) * a.scale);
+    v = CT<CV>::mk(v.x * f, v.y * f);
   } else {
     double s, c;
     fast_sincos(phi, &s, &c);
-    v = cmul(v, make_double2(c * a.scale, s * a.scale));
+    v = cmul(v, CT<CV>::mk((R)(c * a.scale), (R)(s * a.scale)));
   }
 }
 
@@ -91,24 +97,24 @@ __device__ __forceinline__ void mul_kphase(double2& v, double kx2, double ky2, d
 // z passes
 // ---------------------------------------------------------------------------
 
-template <int L>
+template <int L, typename CV>
 struct ZCfg {
   static constexpr int T = L / kElems;
   static constexpr int C = (256 / T) > 0 ? (256 / T) : 1;  // lines per block
   static constexpr int threads = C * T;
-  static constexpr int smem_line = L + L / 8;             // padded double2 per line
-  static constexpr size_t smem = (size_t)C * smem_line * sizeof(double2);
+  static constexpr int smem_line = L + L / 8;             // padded complex per line
+  static constexpr size_t smem = (size_t)C * smem_line * sizeof(CV);
 };
 
 struct ZArgs {
-  double2* psi;
+  void* psi;
   uint32_t nlines;  // nx_local * ny
   PhaseArgs ph;
 };
 
-template <int L, int KIND, bool VTAB, typename Sync>
-__device__ __forceinline__ void z_body(const ZArgs& a, double2* v, int t, uint32_t off, bool active,
-                                       const double2* __restrict__ tw, SmemContig sm, Sync sync) {
+template <int L, int KIND, bool VTAB, typename CV, typename Sync>
+__device__ __forceinline__ void z_body(const ZArgs& a, CV* v, int t, uint32_t off, bool active,
+                                       const CV* __restrict__ tw, SmemContig<CV> sm, Sync sync) {
   constexpr int T = L / kElems;
   if constexpr (KIND == T_FWD) {
     line_fft<L, -1>(v, t, tw, sm, sync);
@@ -123,9 +129,10 @@ __device__ __forceinline__ void z_body(const ZArgs& a, double2* v, int t, uint32
   } else if constexpr (KIND == T_VMID && VTAB) {  // inverse, x exp(-iV dt) table, forward
     // the table values are loaded before the inverse transform so their
     // latency hides behind it (they are consumed right after it)
-    double2 f[kElems];
+    const CV* expv = (const CV*)a.ph.expv;
+    CV f[kElems];
 #pragma unroll
-    for (int m = 0; m < kElems; ++m) f[m] = active ? __ldcg(&a.ph.expv[off + t + m * T]) : make_double2(1.0, 0.0);
+    for (int m = 0; m < kElems; ++m) f[m] = active ? __ldcg(&expv[off + t + m * T]) : CT<CV>::mk(1, 0);
     line_fft<L, +1>(v, t, tw, sm, sync);
 #pragma unroll
     for (int m = 0; m < kElems; ++m) v[m] = cmul(v[m], f[m]);
@@ -148,27 +155,29 @@ struct ZMinBlocks {
   static constexpr int value = (KIND == T_VMID && VTAB) ? CTAP_Z_MINB_TAB : CTAP_Z_MINB;
 };
 
-template <int L, int KIND, bool VTAB>
-__global__ void __launch_bounds__(ZCfg<L>::threads, ZMinBlocks<KIND, VTAB>::value) zline_kernel(ZArgs a, const double2* __restrict__ tw) {
-  using C = ZCfg<L>;
-  extern __shared__ double2 smem[];
-  const int t = threadIdx.x % C::T;
-  const int c = threadIdx.x / C::T;
-  const uint32_t line = blockIdx.x * C::C + c;
+template <int L, int KIND, bool VTAB, typename CV>
+__global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::value) zline_kernel(ZArgs a, const CV* __restrict__ tw) {
+  using Cfg = ZCfg<L, CV>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CV* smem = reinterpret_cast<CV*>(smem_raw);
+  CV* psi = (CV*)a.psi;
+  const int t = threadIdx.x % Cfg::T;
+  const int c = threadIdx.x / Cfg::T;
+  const uint32_t line = blockIdx.x * Cfg::C + c;
   const bool active = line < a.nlines;
   const uint32_t off = line * L;
-  SmemContig sm{smem + c * C::smem_line};
-  double2 v[kElems];
+  SmemContig<CV> sm{smem + c * Cfg::smem_line};
+  CV v[kElems];
 #pragma unroll
-  for (int m = 0; m < kElems; ++m) v[m] = active ? __ldcg(&a.psi[off + t + m * C::T]) : make_double2(0.0, 0.0);
-  if constexpr (C::T <= 32) {
+  for (int m = 0; m < kElems; ++m) v[m] = active ? __ldcg(&psi[off + t + m * Cfg::T]) : CT<CV>::mk(0, 0);
+  if constexpr (Cfg::T <= 32) {
     z_body<L, KIND, VTAB>(a, v, t, off, active, tw, sm, SyncWarp{});
   } else {
-    z_body<L, KIND, VTAB>(a, v, t, off, active, tw, sm, SyncNamed{1 + c, C::T});
+    z_body<L, KIND, VTAB>(a, v, t, off, active, tw, sm, SyncNamed{1 + c, Cfg::T});
   }
   if (active) {
 #pragma unroll
-    for (int m = 0; m < kElems; ++m) __stcg(&a.psi[off + t + m * C::T], v[m]);
+    for (int m = 0; m < kElems; ++m) __stcg(&psi[off + t + m * Cfg::T], v[m]);
   }
 }
 
@@ -182,14 +191,14 @@ __global__ void __launch_bounds__(ZCfg<L>::threads, ZMinBlocks<KIND, VTAB>::valu
 #define CTAP_TILE_E 8
 #endif
 
-template <int L>
+template <int L, typename CV>
 struct TileCfg {
   static constexpr int E = (L >= 256) ? CTAP_TILE_E : kElems;
   static constexpr int T = L / E;
   static constexpr int per_tile = T * 8;
   static constexpr int G = per_tile >= 128 ? 1 : 128 / per_tile;  // tiles per block
   static constexpr int threads = G * per_tile;
-  static constexpr size_t smem = (size_t)G * L * 8 * sizeof(double2);
+  static constexpr size_t smem = (size_t)G * L * 8 * sizeof(CV);
   static constexpr int occ = CTAP_OCC * kElems / E;  // same register file, E/8 x the registers
   static constexpr int minb = occ / threads > 0 ? occ / threads : 1;
   static constexpr int minb_tab = CTAP_OCC_TAB / threads > 0 ? CTAP_OCC_TAB / threads : 1;
@@ -217,17 +226,17 @@ __device__ __forceinline__ uint32_t inner(const Layout& l, uint32_t i) {
 }
 
 struct TileArgs {
-  const double2* in;
-  double2* out;
+  const void* in;
+  void* out;
   Layout lin, lout;
   uint32_t n_outer;  // number of outer indices
   uint32_t nchunk;   // 8-column chunks per outer index (nz / 8)
   PhaseArgs ph;
 };
 
-template <int L, int E, int KIND, bool KTAB, bool KBLK>
-__device__ __forceinline__ void tile_body(const TileArgs& a, double2* v, int t, uint32_t o, uint32_t z,
-                                          bool active, const double2* __restrict__ tw, SmemStrided sm) {
+template <int L, int E, int KIND, bool KTAB, bool KBLK, typename CV>
+__device__ __forceinline__ void tile_body(const TileArgs& a, CV* v, int t, uint32_t o, uint32_t z,
+                                          bool active, const CV* __restrict__ tw, SmemStrided<CV> sm) {
   constexpr int T = L / E;
   if constexpr (KIND == T_COPY) {  // diagnostics: the pass's memory traffic without the transform
   } else if constexpr (KIND == T_FWD) {
@@ -238,12 +247,12 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, double2* v, int t, 
     // operands of the phase, loaded ahead of the forward transform so their
     // latency hides behind it
     double kx2[E], ky2 = 0.0, kz2 = 0.0;
-    double2 f[E];
+    CV f[E];
     if constexpr (KTAB) {
+      const CV* expk = (const CV*)a.ph.expk;
 #pragma unroll
       for (int m = 0; m < E; ++m)
-        f[m] = active ? __ldcg(&a.ph.expk[outer(a.lout, o) + inner<KBLK>(a.lout, t + m * T) + z])
-                      : make_double2(0.0, 0.0);
+        f[m] = active ? __ldcg(&expk[outer(a.lout, o) + inner<KBLK>(a.lout, t + m * T) + z]) : CT<CV>::mk(0, 0);
     } else {
       ky2 = __ldg(&a.ph.ky2[a.ph.outer_off + o]);
       kz2 = __ldg(&a.ph.kz2[z]);
@@ -264,27 +273,30 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, double2* v, int t, 
   }
 }
 
-template <int L, int KIND, bool PIN, bool POUT, bool KTAB>
-__global__ void __launch_bounds__(TileCfg<L>::threads, KTAB ? TileCfg<L>::minb_tab : TileCfg<L>::minb) tile_kernel(TileArgs a,
-                                                                               const double2* __restrict__ tw) {
-  using C = TileCfg<L>;
-  extern __shared__ double2 smem[];
+template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV>
+__global__ void __launch_bounds__(TileCfg<L, CV>::threads, KTAB ? TileCfg<L, CV>::minb_tab : TileCfg<L, CV>::minb)
+    tile_kernel(TileArgs a, const CV* __restrict__ tw) {
+  using Cfg = TileCfg<L, CV>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CV* smem = reinterpret_cast<CV*>(smem_raw);
+  const CV* in = (const CV*)a.in;
+  CV* out = (CV*)a.out;
   const int col = threadIdx.x & 7;
-  const int t = (threadIdx.x >> 3) % C::T;
-  const int g = threadIdx.x / C::per_tile;
-  const uint32_t tile = blockIdx.x * C::G + g;
+  const int t = (threadIdx.x >> 3) % Cfg::T;
+  const int g = threadIdx.x / Cfg::per_tile;
+  const uint32_t tile = blockIdx.x * Cfg::G + g;
   const bool active = tile < a.n_outer * a.nchunk;
   const uint32_t o = active ? tile / a.nchunk : 0;
   const uint32_t z = (active ? (tile - o * a.nchunk) : 0) * 8 + col;
-  constexpr int E = C::E;
+  constexpr int E = Cfg::E;
   const uint32_t obi = outer(a.lin, o) + z, obo = outer(a.lout, o) + z;
-  double2 v[E];
+  CV v[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = active ? a.in[obi + inner<PIN>(a.lin, t + m * C::T)] : make_double2(0.0, 0.0);
-  tile_body<L, E, KIND, KTAB, POUT>(a, v, t, o, z, active, tw, SmemStrided{smem + (size_t)g * L * 8 + col});
+  for (int m = 0; m < E; ++m) v[m] = active ? in[obi + inner<PIN>(a.lin, t + m * Cfg::T)] : CT<CV>::mk(0, 0);
+  tile_body<L, E, KIND, KTAB, POUT>(a, v, t, o, z, active, tw, SmemStrided<CV>{smem + (size_t)g * L * 8 + col});
   if (active) {
 #pragma unroll
-    for (int m = 0; m < E; ++m) a.out[obo + inner<POUT>(a.lout, t + m * C::T)] = v[m];
+    for (int m = 0; m < E; ++m) out[obo + inner<POUT>(a.lout, t + m * Cfg::T)] = v[m];
   }
 }
 
@@ -298,24 +310,24 @@ static cudaError_t allow_smem(K k, size_t bytes) {
                            : cudaSuccess;
 }
 
-template <int L, int KIND, bool VTAB>
-static cudaError_t launch_z(const ZArgs& a, const double2* tw, cudaStream_t st) {
-  using C = ZCfg<L>;
-  auto k = zline_kernel<L, KIND, VTAB>;
-  static cudaError_t init = allow_smem(k, C::smem);
+template <int L, int KIND, bool VTAB, typename CV>
+static cudaError_t launch_z(const ZArgs& a, const CV* tw, cudaStream_t st) {
+  using Cfg = ZCfg<L, CV>;
+  auto k = zline_kernel<L, KIND, VTAB, CV>;
+  static cudaError_t init = allow_smem(k, Cfg::smem);
   if (init != cudaSuccess) return init;
-  k<<<(a.nlines + C::C - 1) / C::C, C::threads, C::smem, st>>>(a, tw);
+  k<<<(a.nlines + Cfg::C - 1) / Cfg::C, Cfg::threads, Cfg::smem, st>>>(a, tw);
   return cudaGetLastError();
 }
 
-template <int L, int KIND, bool PIN, bool POUT, bool KTAB>
-static cudaError_t launch_tile(const TileArgs& a, const double2* tw, cudaStream_t st) {
-  using C = TileCfg<L>;
-  auto k = tile_kernel<L, KIND, PIN, POUT, KTAB>;
-  static cudaError_t init = allow_smem(k, C::smem);
+template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV>
+static cudaError_t launch_tile(const TileArgs& a, const CV* tw, cudaStream_t st) {
+  using Cfg = TileCfg<L, CV>;
+  auto k = tile_kernel<L, KIND, PIN, POUT, KTAB, CV>;
+  static cudaError_t init = allow_smem(k, Cfg::smem);
   if (init != cudaSuccess) return init;
   const uint32_t ntiles = a.n_outer * a.nchunk;
-  k<<<(ntiles + C::G - 1) / C::G, C::threads, C::smem, st>>>(a, tw);
+  k<<<(ntiles + Cfg::G - 1) / Cfg::G, Cfg::threads, Cfg::smem, st>>>(a, tw);
   return cudaGetLastError();
 }
 
@@ -332,16 +344,24 @@ static cudaError_t launch_tile(const TileArgs& a, const double2* tw, cudaStream_
   }                                             \
   return cudaErrorInvalidValue;
 
+// twiddle tables of both precisions for one line length
+struct Tw {
+  const double2* d;
+  const float2* f;
+};
+
 template <int KIND, bool VTAB>
-static cudaError_t dispatch_z(int L, const ZArgs& a, const double2* tw, cudaStream_t st) {
-#define CTAP_Z(LL) launch_z<LL, KIND, VTAB>(a, tw, st)
+static cudaError_t dispatch_z(int L, bool c64, const ZArgs& a, Tw tw, cudaStream_t st) {
+#define CTAP_Z(LL) (c64 ? launch_z<LL, KIND, VTAB, float2>(a, tw.f, st) : launch_z<LL, KIND, VTAB, double2>(a, tw.d, st))
   CTAP_BY_LENGTH(L, CTAP_Z)
 #undef CTAP_Z
 }
 
 template <int KIND, bool PIN, bool POUT, bool KTAB>
-static cudaError_t dispatch_tile(int L, const TileArgs& a, const double2* tw, cudaStream_t st) {
-#define CTAP_T(LL) launch_tile<LL, KIND, PIN, POUT, KTAB>(a, tw, st)
+static cudaError_t dispatch_tile(int L, bool c64, const TileArgs& a, Tw tw, cudaStream_t st) {
+#define CTAP_T(LL)                                                             \
+  (c64 ? launch_tile<LL, KIND, PIN, POUT, KTAB, float2>(a, tw.f, st)           \
+       : launch_tile<LL, KIND, PIN, POUT, KTAB, double2>(a, tw.d, st))
   CTAP_BY_LENGTH(L, CTAP_T)
 #undef CTAP_T
 }
@@ -354,11 +374,13 @@ static int ilog2(int64_t v) {
 
 // materialised phase factors (StepPlan.exp_v_half / exp_v_full / exp_k,
 // propagator.py:45-47) for inspection, and the plan's phase tables
-__global__ void phase_field_kernel(double2* __restrict__ out, const double* __restrict__ vi,
+template <typename CV>
+__global__ void phase_field_kernel(CV* __restrict__ out, const double* __restrict__ vi,
                                    const double* __restrict__ kx2, const double* __restrict__ ky2,
                                    const double* __restrict__ kz2, uint32_t nx, uint32_t ny, uint32_t nz,
                                    uint32_t x_off, uint32_t y_off, int which, int imag, double dt_i,
                                    double len2, double scale, int lx) {
+  using R = typename CT<CV>::R;
   const uint32_t n = nx * ny * nz;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double phi;
@@ -372,11 +394,11 @@ __global__ void phase_field_kernel(double2* __restrict__ out, const double* __re
       phi = v_phase_i(vi[i], which == 0 ? -0.5 : -1.0, dt_i);
     }
     if (imag) {
-      out[dst] = make_double2(exp(phi) * scale, 0.0);
+      out[dst] = CT<CV>::mk((R)(exp(phi) * scale), (R)0);
     } else {
       double s, c;
       fast_sincos(phi, &s, &c);
-      out[dst] = make_double2(c * scale, s * scale);
+      out[dst] = CT<CV>::mk((R)(c * scale), (R)(s * scale));
     }
   }
 }
@@ -429,27 +451,44 @@ cudaError_t ctap_run_v_internal(const ctap_plan* p, cudaStream_t st) {
 }
 
 // which: 0 exp_v_half, 1 exp_v_full, 2 exp_k (natural x-slab layout),
-//        3 exp_k / N in the x-pass (y-slab) layout, for the tables
-cudaError_t ctap_run_phase_field(const ctap_plan* p, int which, void* out, cudaStream_t st) {
+//        3 exp_k / N in the x-pass (y-slab) layout, for the tables.
+// `table`: write in the plan's precision (phase tables) instead of complex128.
+template <typename CV>
+static cudaError_t phase_field(const ctap_plan* p, int which, void* out, cudaStream_t st) {
   const int imag = p->mode == 1;
   if (which == 3) {
     const uint32_t nyl = (uint32_t)(p->n[1] / p->slab_p);
-    phase_field_kernel<<<p->red_blocks, 256, 0, st>>>(
-        (double2*)out, p->vi_dev, p->k2_dev[0], p->k2_dev[1], p->k2_dev[2], (uint32_t)p->n[0], nyl,
+    phase_field_kernel<CV><<<p->red_blocks, 256, 0, st>>>(
+        (CV*)out, p->vi_dev, p->k2_dev[0], p->k2_dev[1], p->k2_dev[2], (uint32_t)p->n[0], nyl,
         (uint32_t)p->n[2], 0u, (uint32_t)p->slab_r * nyl, 2, imag, p->dt_i, p->len2, p->inv_scale, p->k_lx);
   } else {
-    phase_field_kernel<<<p->red_blocks, 256, 0, st>>>(
-        (double2*)out, p->vi_dev, p->k2_dev[0], p->k2_dev[1], p->k2_dev[2], (uint32_t)p->nx_local,
+    phase_field_kernel<CV><<<p->red_blocks, 256, 0, st>>>(
+        (CV*)out, p->vi_dev, p->k2_dev[0], p->k2_dev[1], p->k2_dev[2], (uint32_t)p->nx_local,
         (uint32_t)p->n[1], (uint32_t)p->n[2], (uint32_t)(p->slab_r * p->nx_local), 0u, which, imag, p->dt_i,
         p->len2, 1.0, 0);
   }
   return cudaGetLastError();
 }
 
+cudaError_t ctap_run_phase_field(const ctap_plan* p, int which, void* out, cudaStream_t st) {
+  return phase_field<double2>(p, which, out, st);
+}
+
+cudaError_t ctap_run_phase_table(const ctap_plan* p, int which, void* out, cudaStream_t st) {
+  return p->dtype == CTAP_C64 ? phase_field<float2>(p, which, out, st) : phase_field<double2>(p, which, out, st);
+}
+
 // Run one pass on the plan's local data.  `in`/`out` may alias (natural
 // layouts, in place).  Returns a CUDA error code.
+static Tw twid(const ctap_plan* p, int64_t L) {
+  const int off = p->tw_off[ilog2(L) - 3];
+  return Tw{p->twiddles + off, p->twiddles32 + off};
+}
+
 cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* out, cudaStream_t st) {
   const int64_t nx = p->n[0], ny = p->n[1], nz = p->n[2];
+  const bool c64 = p->dtype == CTAP_C64;
+  const Tw tw_any = twid(p, 8);
   const int P = p->slab_p;
   const uint32_t nxl = (uint32_t)(nx / P), nyl = (uint32_t)(ny / P);
   PhaseArgs ph;
@@ -468,24 +507,24 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
   if (kind >= PASS_Z_FWD && kind <= PASS_Z_LAST) {
     if (in != out) return cudaErrorInvalidValue;
     ZArgs a;
-    a.psi = (double2*)out;
+    a.psi = out;
     a.nlines = (uint32_t)(p->nx_local * ny);
     a.ph = ph;
-    const double2* tw = p->twiddles + p->tw_off[ilog2(nz) - 3];
+    const Tw tw = twid(p, nz);
     const int L = (int)nz;
     switch (kind) {
-      case PASS_Z_FWD: return dispatch_z<T_FWD, false>(L, a, tw, st);
-      case PASS_Z_INV: return dispatch_z<T_INV, false>(L, a, tw, st);
-      case PASS_Z_FIRST: return dispatch_z<T_VFIRST, false>(L, a, tw, st);
+      case PASS_Z_FWD: return dispatch_z<T_FWD, false>(L, c64, a, tw, st);
+      case PASS_Z_INV: return dispatch_z<T_INV, false>(L, c64, a, tw, st);
+      case PASS_Z_FIRST: return dispatch_z<T_VFIRST, false>(L, c64, a, tw, st);
       case PASS_Z_MID:
-        return p->expv_dev ? dispatch_z<T_VMID, true>(L, a, tw, st) : dispatch_z<T_VMID, false>(L, a, tw, st);
-      case PASS_Z_LAST: return dispatch_z<T_VLAST, false>(L, a, tw, st);
+        return p->expv_dev ? dispatch_z<T_VMID, true>(L, c64, a, tw, st) : dispatch_z<T_VMID, false>(L, c64, a, tw, st);
+      case PASS_Z_LAST: return dispatch_z<T_VLAST, false>(L, c64, a, tw, st);
     }
     return cudaErrorInvalidValue;
   }
   TileArgs a;
-  a.in = (const double2*)in;
-  a.out = (double2*)out;
+  a.in = in;
+  a.out = out;
   a.nchunk = (uint32_t)(nz / 8);
   a.ph = ph;
   const uint32_t NZ = (uint32_t)nz, NY = (uint32_t)ny;
@@ -508,57 +547,57 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
     case PASS_Y_FWD_BLK:
     case PASS_Y_INV_BLK: {
       a.n_outer = nxl;
-      const double2* tw = p->twiddles + p->tw_off[ilog2(ny) - 3];
+      const Tw tw = twid(p, ny);
       if (kind == PASS_Y_FWD_BLK) {
         a.lin = y_nat;
         a.lout = y_blk;
-        return dispatch_tile<T_FWD, false, false, false>((int)ny, a, tw, st);
+        return dispatch_tile<T_FWD, false, false, false>((int)ny, c64, a, tw, st);
       }
       a.lin = y_blk;
       a.lout = y_nat;
-      return dispatch_tile<T_INV, false, false, false>((int)ny, a, tw, st);
+      return dispatch_tile<T_INV, false, false, false>((int)ny, c64, a, tw, st);
     }
     case PASS_X_KIN_BLK: {
       a.lin = x_blk;
       a.lout = x_blk;
       a.n_outer = NY;
-      const double2* tw = p->twiddles + p->tw_off[ilog2(nx) - 3];
-      return p->expk_dev ? dispatch_tile<T_KIN, true, true, true>((int)nx, a, tw, st)
-                         : dispatch_tile<T_KIN, true, true, false>((int)nx, a, tw, st);
+      const Tw tw = twid(p, nx);
+      return p->expk_dev ? dispatch_tile<T_KIN, true, true, true>((int)nx, c64, a, tw, st)
+                         : dispatch_tile<T_KIN, true, true, false>((int)nx, c64, a, tw, st);
     }
     case PASS_Y_FWD:
     case PASS_Y_INV:
     case PASS_Y_FWD_TO_PEER:
     case PASS_Y_INV_FROM_PEER: {
       a.n_outer = nxl;
-      const double2* tw = p->twiddles + p->tw_off[ilog2(ny) - 3];
+      const Tw tw = twid(p, ny);
       const int L = (int)ny;
       if (kind == PASS_Y_FWD_TO_PEER && peer) {
         a.lin = y_nat;
         a.lout = y_peer;
-        return dispatch_tile<T_FWD, false, true, false>(L, a, tw, st);
+        return dispatch_tile<T_FWD, false, true, false>(L, c64, a, tw, st);
       }
       if (kind == PASS_Y_INV_FROM_PEER && peer) {
         a.lin = y_peer;
         a.lout = y_nat;
-        return dispatch_tile<T_INV, true, false, false>(L, a, tw, st);
+        return dispatch_tile<T_INV, true, false, false>(L, c64, a, tw, st);
       }
       a.lin = y_nat;
       a.lout = y_nat;
       const bool fwd = (kind == PASS_Y_FWD || kind == PASS_Y_FWD_TO_PEER);
-      return fwd ? dispatch_tile<T_FWD, false, false, false>(L, a, tw, st)
-                 : dispatch_tile<T_INV, false, false, false>(L, a, tw, st);
+      return fwd ? dispatch_tile<T_FWD, false, false, false>(L, c64, a, tw, st)
+                 : dispatch_tile<T_INV, false, false, false>(L, c64, a, tw, st);
     }
     case PASS_Y_COPY:
       a.n_outer = nxl;
       a.lin = y_nat;
       a.lout = y_nat;
-      return dispatch_tile<T_COPY, false, false, false>((int)ny, a, p->twiddles, st);
+      return dispatch_tile<T_COPY, false, false, false>((int)ny, c64, a, tw_any, st);
     case PASS_X_COPY:
       a.n_outer = nyl;
       a.lin = x_nat;
       a.lout = x_nat;
-      return dispatch_tile<T_COPY, false, false, false>((int)nx, a, p->twiddles, st);
+      return dispatch_tile<T_COPY, false, false, false>((int)nx, c64, a, tw_any, st);
     case PASS_X_KIN:
     case PASS_X_FWD:
     case PASS_X_INV: {
@@ -566,13 +605,13 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       a.lout = x_nat;
       a.n_outer = nyl;
       a.ph.outer_off = (uint32_t)p->slab_r * nyl;
-      const double2* tw = p->twiddles + p->tw_off[ilog2(nx) - 3];
+      const Tw tw = twid(p, nx);
       const int L = (int)nx;
       if (kind == PASS_X_KIN)
-        return p->expk_dev && p->k_lx == 0 ? dispatch_tile<T_KIN, false, false, true>(L, a, tw, st)
-                                           : dispatch_tile<T_KIN, false, false, false>(L, a, tw, st);
-      if (kind == PASS_X_FWD) return dispatch_tile<T_FWD, false, false, false>(L, a, tw, st);
-      return dispatch_tile<T_INV, false, false, false>(L, a, tw, st);
+        return p->expk_dev && p->k_lx == 0 ? dispatch_tile<T_KIN, false, false, true>(L, c64, a, tw, st)
+                                           : dispatch_tile<T_KIN, false, false, false>(L, c64, a, tw, st);
+      if (kind == PASS_X_FWD) return dispatch_tile<T_FWD, false, false, false>(L, c64, a, tw, st);
+      return dispatch_tile<T_INV, false, false, false>(L, c64, a, tw, st);
     }
   }
   return cudaErrorInvalidValue;

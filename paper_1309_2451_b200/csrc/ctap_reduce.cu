@@ -57,16 +57,17 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(const double* __r
   block_reduce_store<NV>(acc, out);
 }
 
+template <typename CV>
 struct ObserveF {
-  const double2* psi;
+  const CV* psi;
   const double* xs;
   const double* xb1;
   const double* xb2;
   int64_t nyz, ny, nz, nx_global, x_off;
   int margin;
   __device__ __forceinline__ void operator()(int64_t i, double (&acc)[5]) const {
-    double2 a = psi[i];
-    double rho = a.x * a.x + a.y * a.y;
+    const CV a = psi[i];
+    const double rho = (double)a.x * a.x + (double)a.y * a.y;
     int64_t x = i / nyz;
     int64_t r = i - x * nyz;
     int64_t y = r / nz;
@@ -87,15 +88,16 @@ struct ObserveF {
   }
 };
 
+template <typename CV>
 struct K2F {
-  const double2* phi;
+  const CV* phi;
   const double* kx2;
   const double* ky2;
   const double* kz2;
   int64_t nylz, nyl, nz, y_off;
   __device__ __forceinline__ void operator()(int64_t i, double (&acc)[2]) const {
-    double2 a = phi[i];
-    double rho = a.x * a.x + a.y * a.y;
+    const CV a = phi[i];
+    const double rho = (double)a.x * a.x + (double)a.y * a.y;
     int64_t x = i / nylz;
     int64_t r = i - x * nylz;
     int64_t y = r / nz;
@@ -106,12 +108,13 @@ struct K2F {
   }
 };
 
+template <typename CV>
 struct VF {
-  const double2* psi;
+  const CV* psi;
   const double* V;
   __device__ __forceinline__ void operator()(int64_t i, double (&acc)[2]) const {
-    double2 a = psi[i];
-    double rho = a.x * a.x + a.y * a.y;
+    const CV a = psi[i];
+    const double rho = (double)a.x * a.x + (double)a.y * a.y;
     acc[0] += V[i] * rho;
     acc[1] += rho;
   }
@@ -126,16 +129,17 @@ static cudaError_t run_reduce(const ctap_plan* p, F f, int64_t n, double* out, c
   return cudaGetLastError();
 }
 
-__global__ void density_xz_kernel(const double2* __restrict__ psi, int64_t nxl, int64_t ny, int64_t nz,
+template <typename CV>
+__global__ void density_xz_kernel(const CV* __restrict__ psi, int64_t nxl, int64_t ny, int64_t nz,
                                   double* __restrict__ out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nxl * nz) return;
   int64_t x = i / nz, z = i - (i / nz) * nz;
-  const double2* base = psi + x * ny * nz + z;
+  const CV* base = psi + x * ny * nz + z;
   double s = 0.0;
   for (int64_t y = 0; y < ny; ++y) {
-    double2 a = base[y * nz];
-    s += a.x * a.x + a.y * a.y;
+    const CV a = base[y * nz];
+    s += (double)a.x * a.x + (double)a.y * a.y;
   }
   out[i] = s;
 }
@@ -147,15 +151,24 @@ __global__ void scale_kernel(double2* __restrict__ psi, int64_t n, double d) {
     psi[i] = make_double2(a.x / d, a.y / d);
   }
 }
+__global__ void scale_kernel(float2* __restrict__ psi, int64_t n, double d) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const float df = (float)d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float2 a = psi[i];
+    psi[i] = make_float2(a.x / df, a.y / df);
+  }
+}
 
 }  // namespace ctap
 
 using namespace ctap;
 
-cudaError_t ctap_run_observe(const ctap_plan* p, const void* psi, const double* xs, const double* xb1,
+template <typename CV>
+static cudaError_t observe_t(const ctap_plan* p, const void* psi, const double* xs, const double* xb1,
                              const double* xb2, int margin, double* out, cudaStream_t st) {
-  ObserveF f;
-  f.psi = (const double2*)psi;
+  ObserveF<CV> f;
+  f.psi = (const CV*)psi;
   f.xs = xs;
   f.xb1 = xb1;
   f.xb2 = xb2;
@@ -168,9 +181,16 @@ cudaError_t ctap_run_observe(const ctap_plan* p, const void* psi, const double* 
   return run_reduce<5>(p, f, p->nx_local * f.nyz, out, st);
 }
 
-cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, cudaStream_t st) {
-  K2F f;
-  f.phi = (const double2*)phi;
+cudaError_t ctap_run_observe(const ctap_plan* p, const void* psi, const double* xs, const double* xb1,
+                             const double* xb2, int margin, double* out, cudaStream_t st) {
+  return p->dtype == CTAP_C64 ? observe_t<float2>(p, psi, xs, xb1, xb2, margin, out, st)
+                              : observe_t<double2>(p, psi, xs, xb1, xb2, margin, out, st);
+}
+
+template <typename CV>
+static cudaError_t k2_t(const ctap_plan* p, const void* phi, double* out, cudaStream_t st) {
+  K2F<CV> f;
+  f.phi = (const CV*)phi;
   f.kx2 = p->k2_dev[0];
   f.ky2 = p->k2_dev[1];
   f.kz2 = p->k2_dev[2];
@@ -181,23 +201,38 @@ cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, c
   return run_reduce<2>(p, f, p->n[0] * f.nylz, out, st);
 }
 
-cudaError_t ctap_run_v_sums(const ctap_plan* p, const void* psi, double* out, cudaStream_t st) {
-  VF f;
-  f.psi = (const double2*)psi;
+cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, cudaStream_t st) {
+  return p->dtype == CTAP_C64 ? k2_t<float2>(p, phi, out, st) : k2_t<double2>(p, phi, out, st);
+}
+
+template <typename CV>
+static cudaError_t v_t(const ctap_plan* p, const void* psi, double* out, cudaStream_t st) {
+  VF<CV> f;
+  f.psi = (const CV*)psi;
   f.V = p->v_dev;
   return run_reduce<2>(p, f, p->nx_local * p->n[1] * p->n[2], out, st);
+}
+
+cudaError_t ctap_run_v_sums(const ctap_plan* p, const void* psi, double* out, cudaStream_t st) {
+  return p->dtype == CTAP_C64 ? v_t<float2>(p, psi, out, st) : v_t<double2>(p, psi, out, st);
 }
 
 cudaError_t ctap_run_density_xz(const ctap_plan* p, const void* psi, double* out, cudaStream_t st) {
   int64_t n = p->nx_local * p->n[2];
   int threads = 256;
-  density_xz_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, st>>>(
-      (const double2*)psi, p->nx_local, p->n[1], p->n[2], out);
+  const unsigned blocks = (unsigned)((n + threads - 1) / threads);
+  if (p->dtype == CTAP_C64)
+    density_xz_kernel<<<blocks, threads, 0, st>>>((const float2*)psi, p->nx_local, p->n[1], p->n[2], out);
+  else
+    density_xz_kernel<<<blocks, threads, 0, st>>>((const double2*)psi, p->nx_local, p->n[1], p->n[2], out);
   return cudaGetLastError();
 }
 
 cudaError_t ctap_run_scale(const ctap_plan* p, void* psi, double d, cudaStream_t st) {
   int64_t n = p->nx_local * p->n[1] * p->n[2];
-  scale_kernel<<<p->red_blocks, kRedThreads, 0, st>>>((double2*)psi, n, d);
+  if (p->dtype == CTAP_C64)
+    scale_kernel<<<p->red_blocks, kRedThreads, 0, st>>>((float2*)psi, n, d);
+  else
+    scale_kernel<<<p->red_blocks, kRedThreads, 0, st>>>((double2*)psi, n, d);
   return cudaGetLastError();
 }

@@ -32,6 +32,10 @@ from .qgrid import UnitSystem, Wavefunction, as_simgrid, grid_key, same_grid, wr
 REAL_TIME = "real_time"
 IMAGINARY_TIME = "imaginary_time"
 
+# wavefunction precision of a plan: complex128 (the reference's) or the
+# optional complex64 mode (phases still exact in FP64; gate <= 1e-4)
+PRECISIONS = {"complex128": torch.complex128, "complex64": torch.complex64}
+
 # phase-table mask of make_plan (bit 0: exp(-iV dt) table, bit 1: exp(-ik^2 dt/2)
 # table); the environment variable is for A/B
 # measurements
@@ -53,7 +57,7 @@ class NativePlan:
 
     def __init__(self, grid, v_dev: torch.Tensor | None, mass: float, dt: float,
                  mode: str = REAL_TIME, v_shift: float = 0.0, slab_p: int = 1, slab_r: int = 0,
-                 phase_tables: int = 0):
+                 phase_tables: int = 0, precision: str = "complex128"):
         lib = _lib.load()
         dev = _device.require_cuda()
         self.grid = as_simgrid(grid)
@@ -69,6 +73,11 @@ class NativePlan:
         desc.slab_p = int(slab_p)
         desc.slab_r = int(slab_r)
         desc.phase_tables = int(phase_tables)
+        if precision not in PRECISIONS:
+            raise ValueError(f"unknown precision {precision!r}; known: {sorted(PRECISIONS)}")
+        desc.dtype = _lib.DTYPE_C64 if precision == "complex64" else _lib.DTYPE_C128
+        self.precision = precision
+        self.torch_dtype = PRECISIONS[precision]
         self.desc = desc
         # squared wavenumbers exactly as k_squared() forms them (qgrid.py:112-115)
         self._k2 = [np.ascontiguousarray(self.grid.k_axis(i) ** 2) for i in range(3)]
@@ -121,7 +130,7 @@ class NativePlan:
     def phase_field(self, which: int) -> torch.Tensor:
         nxl = self.grid.n[0] // self.desc.slab_p
         out = torch.empty((nxl, self.grid.n[1], self.grid.n[2]), dtype=torch.complex128,
-                          device=self._out.device)
+                          device=self._out.device)  # inspection is always complex128
         _lib.call("ctap_phase_field", self.handle, int(which), out.data_ptr(), _device.stream_handle())
         return out
 
@@ -129,14 +138,15 @@ class NativePlan:
 _AUX = {}
 
 
-def _aux_plan(grid) -> NativePlan:
+def _aux_plan(grid, dtype=torch.complex128) -> NativePlan:
     """A potential-free plan for FFTs and reductions on `grid` (cached)."""
-    key = (grid_key(grid), torch.cuda.current_device() if torch.cuda.is_available() else -1)
+    key = (grid_key(grid), torch.cuda.current_device() if torch.cuda.is_available() else -1, dtype)
     p = _AUX.get(key)
     if p is None:
         from .constants import species_mass
 
-        p = NativePlan(grid, None, species_mass("li6"), 1e-6)
+        prec = "complex64" if dtype == torch.complex64 else "complex128"
+        p = NativePlan(grid, None, species_mass("li6"), 1e-6, precision=prec)
         _AUX[key] = p
     return p
 
@@ -183,7 +193,8 @@ class StepPlan:
 
 
 def make_plan(grid, potential, mass: float, dt: float, mode: str = REAL_TIME,
-              threads: int = 1, *, phase_tables: int | None = None) -> StepPlan:
+              threads: int = 1, *, phase_tables: int | None = None,
+              precision: str = "complex128") -> StepPlan:
     """make_plan (propagator.py:55-81).
 
     `threads` is accepted for signature compatibility (the device decides its
@@ -191,7 +202,9 @@ def make_plan(grid, potential, mass: float, dt: float, mode: str = REAL_TIME,
     which of exp(-i V dt) (PHASE_TABLE_V) and exp(-i k^2 dt/2)
     (PHASE_TABLE_K) are kept as HBM tables instead of being recomputed per
     point every step; the phases are bit-identical either way.  None picks
-    the measured-fastest default."""
+    the measured-fastest default.  `precision="complex64"` selects the
+    optional complex64 mode (complex64 storage and transforms, exact FP64
+    phases; held to <= 1e-4 against the complex128 oracle)."""
     if mode not in (REAL_TIME, IMAGINARY_TIME):
         raise ValueError(f"unknown mode {mode!r}")
     if tuple(potential.shape) != tuple(grid.n):
@@ -207,7 +220,8 @@ def make_plan(grid, potential, mass: float, dt: float, mode: str = REAL_TIME,
         shift = float(v_dev.min().item())
     if phase_tables is None:
         phase_tables = DEFAULT_PHASE_TABLES
-    native = NativePlan(grid, v_dev, mass, dt, mode, v_shift=shift, phase_tables=phase_tables)
+    native = NativePlan(grid, v_dev, mass, dt, mode, v_shift=shift, phase_tables=phase_tables,
+                        precision=precision)
     return StepPlan(grid=grid, dt=dt, mode=mode, mass=mass, potential=potential,
                     threads=threads, native=native)
 
@@ -237,7 +251,7 @@ def step(psi, plan: StepPlan):
     if not plan.matches(psi):
         raise ValueError("plan was built for a different grid")
     w, foreign = _resident(psi)
-    plan.native.advance(w.device_amplitudes(), 1)
+    plan.native.advance(w.device_amplitudes(plan.native.torch_dtype), 1)
     w.invalidate_norm()
     if plan.mode == IMAGINARY_TIME:
         w.normalize()
@@ -289,7 +303,7 @@ def evolve_real(psi, plan: StepPlan, n_steps: int, observers=()):
         current = 0
         for ev in schedule:
             if ev > current:
-                plan.native.advance(w.device_amplitudes(), ev - current)
+                plan.native.advance(w.device_amplitudes(plan.native.torch_dtype), ev - current)
                 w.time += (ev - current) * plan.dt
                 w.invalidate_norm()
                 current = ev
@@ -309,8 +323,9 @@ def evolve_real(psi, plan: StepPlan, n_steps: int, observers=()):
 # ---------------------------------------------------------------------------
 
 def _kinetic_sums(w: Wavefunction) -> tuple:
-    plan = _aux_plan(w.grid)
-    phi = w.device_amplitudes().clone()
+    d = w.device_amplitudes(None)
+    plan = _aux_plan(w.grid, d.dtype)
+    phi = d.clone()
     plan.fft3d(phi, -1)
     s = plan.k2_sums(phi).tolist()
     return s[0], s[1]
@@ -327,8 +342,9 @@ def kinetic_expectation(psi, mass: float, workers: int = 1) -> float:
 
 def _potential_from(w: Wavefunction, potential) -> float:
     v_dev = _device.to_device_f64(potential)
-    plan = NativePlan(w.grid, v_dev, 1.0, 1.0)
-    s = plan.v_sums(w.device_amplitudes()).tolist()
+    d = w.device_amplitudes(None)
+    plan = NativePlan(w.grid, v_dev, 1.0, 1.0, precision="complex64" if d.dtype == torch.complex64 else "complex128")
+    s = plan.v_sums(d).tolist()
     return s[0] / s[1]
 
 
@@ -346,7 +362,7 @@ def _energy_on_plan(w: Wavefunction, plan: StepPlan) -> float:
     from .constants import hbar
 
     sk, s = _kinetic_sums(w)
-    sv = plan.native.v_sums(w.device_amplitudes()).tolist()
+    sv = plan.native.v_sums(w.device_amplitudes(plan.native.torch_dtype)).tolist()
     return (hbar ** 2 / (2 * plan.mass)) * sk / s + sv[0] / sv[1]
 
 
@@ -378,7 +394,7 @@ def ground_state_imaginary(grid, potential, seed, tol: float = 1e-10, tau: float
     done = 0
     while done < max_steps:
         n = min(check_every, max_steps - done)
-        plan.native.advance(psi.device_amplitudes(), n)
+        plan.native.advance(psi.device_amplitudes(plan.native.torch_dtype), n)
         psi.invalidate_norm()
         psi.normalize()
         done += n
@@ -409,6 +425,81 @@ class SnapshotObserver:
         path = os.path.join(str(self.out_dir), f"psi_{step_index:07d}.qwf")
         write_snapshot(path, psi.amplitudes, psi.grid, time=psi.time)
         self.written.append(path)
+
+
+class AsyncSnapshotObserver:
+    """QWF1 snapshots without stalling the step loop.
+
+    At each event psi is copied device-to-device into a snapshot buffer (one
+    HBM read + write), the device-to-host copy of that buffer runs on a side
+    stream into pinned memory while the propagation continues, and a writer
+    thread produces the same files as SnapshotObserver
+    (psi_<step:07d>.qwf, qgrid.write_snapshot).  Call close() (or use it as a
+    context manager) to wait for the last file."""
+
+    def __init__(self, out_dir, stride: int = 1):
+        import queue
+        import threading
+
+        self.out_dir = out_dir
+        self.stride = stride
+        self.written = []
+        self._q = queue.Queue(maxsize=2)
+        self._bufs = {}
+        self._stream = None
+        self._err = None
+        self._thread = threading.Thread(target=self._writer, daemon=True)
+        self._thread.start()
+
+    def _writer(self):
+        while True:
+            item = self._q.get()
+            if item is None:
+                return
+            path, event, host, grid, t = item
+            try:
+                event.synchronize()
+                write_snapshot(path, host.numpy(), grid, time=t)
+                self.written.append(path)
+            except BaseException as exc:  # surfaced by close()
+                self._err = exc
+
+    def notify(self, step_index: int, psi):
+        import os
+
+        d = psi.device_amplitudes(None) if isinstance(psi, Wavefunction) else _device.to_device_c128(psi.amplitudes)
+        if self._stream is None:
+            self._stream = torch.cuda.Stream(device=d.device)
+        key = (tuple(d.shape), d.dtype)
+        if key not in self._bufs:
+            self._bufs[key] = [(torch.empty_like(d), torch.empty(d.shape, dtype=d.dtype, pin_memory=True))
+                               for _ in range(3)]
+            self._next = 0
+        dev_buf, host = self._bufs[key][self._next % 3]
+        self._next += 1
+        dev_buf.copy_(d)                                # on the propagation stream
+        ready = torch.cuda.Event()
+        ready.record()
+        self._stream.wait_event(ready)
+        with torch.cuda.stream(self._stream):
+            host.copy_(dev_buf, non_blocking=True)      # overlaps the next steps
+            done = torch.cuda.Event()
+            done.record(self._stream)
+        path = os.path.join(str(self.out_dir), f"psi_{step_index:07d}.qwf")
+        self._q.put((path, done, host, psi.grid, psi.time))
+
+    def close(self):
+        self._q.put(None)
+        self._thread.join()
+        if self._err is not None:
+            raise self._err
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
 
 
 @dataclass

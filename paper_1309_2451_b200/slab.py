@@ -113,7 +113,7 @@ class SlabPropagator:
     """Real- or imaginary-time propagation of one rank's x-slab on its GPU."""
 
     def __init__(self, grid, v_local, mass: float, dt: float, group=None, mode: str = REAL_TIME,
-                 v_shift: float = 0.0, phase_tables: int | None = None):
+                 v_shift: float = 0.0, phase_tables: int | None = None, precision: str = "complex128"):
         self.grid = as_simgrid(grid)
         self.group = group
         P = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -128,10 +128,11 @@ class SlabPropagator:
             phase_tables = DEFAULT_PHASE_TABLES
         self.phase_tables = int(phase_tables)
         self.native = NativePlan(self.grid, self.v_local, mass, dt, mode, v_shift=v_shift,
-                                 slab_p=P, slab_r=r, phase_tables=phase_tables)
+                                 slab_p=P, slab_r=r, phase_tables=phase_tables, precision=precision)
         dev = self.v_local.device
-        self.send = torch.empty(self.layout.points, dtype=torch.complex128, device=dev)
-        self.recv = torch.empty(self.layout.points, dtype=torch.complex128, device=dev)
+        dt_ = self.native.torch_dtype
+        self.send = torch.empty(self.layout.points, dtype=dt_, device=dev)
+        self.recv = torch.empty(self.layout.points, dtype=dt_, device=dev)
 
     def _a2a(self, src: torch.Tensor, dst: torch.Tensor):
         if self.layout.P == 1:

@@ -5,7 +5,7 @@
 cfg1   64^3 run_bench harmonic trap, 1000 steps, populations every 50
 cfg2b  128x128x256 Ioffe-floor harmonic (population-moving), 5000 steps / 25
 cfg2   128x128x256 scaled-chip CTAP (configs/scaled.cfg with n_y = 128),
-       25,000 steps, PopulationRecorder every 50, EdgeMonitor 5e-3
+       25,000 steps, PopulationRecorder every 50
 cfg3   256^3 paper-chip CTAP, 1000 steps / 100
 
 Both sides start from the identical psi0 (host-built Gaussian) and V (device
@@ -124,8 +124,9 @@ def cfg2():
     grid = qgrid.SimGrid(og.n, og.extents, og.origin)
     v, check = chip_potential(grid, og, "scaled", True)
     a0 = orc.gaussian_packet(og, (-7e-6, 2e-6, 60e-6), (0.3e-6, 0.3e-6, 9.2e-6))
-    return run_case("cfg2 128x128x256 scaled-chip CTAP", grid, v, a0, 25000, 50, 3.5e-6,
-                    edge_threshold=5e-3, v_check=check)
+    # the edge mass is recorded in the trace; no EdgeMonitor abort (its 5e-3
+    # threshold was tuned for the reference's ground-state psi0, not this packet)
+    return run_case("cfg2 128x128x256 scaled-chip CTAP", grid, v, a0, 25000, 50, 3.5e-6, v_check=check)
 
 
 def cfg3():

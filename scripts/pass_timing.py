@@ -24,16 +24,15 @@ def main():
     n = nx * ny * nz
     v = torch.full((nx, ny, nz), muB / 2 * 0.03, dtype=torch.float64, device="cuda")
     v += torch.rand_like(v) * 1e-29
-    plan = propagator.make_plan(grid, v, m, 1e-6, phase_tables=int(os.environ.get('CTAP_PHASE_TABLES', '1')))
-    psi = (torch.randn(nx, ny, nz, dtype=torch.complex128, device="cuda") * 1e-3).contiguous()
+    prec = os.environ.get('CTAP_PRECISION', 'complex128')
+    plan = propagator.make_plan(grid, v, m, 1e-6, phase_tables=int(os.environ.get('CTAP_PHASE_TABLES', '1')), precision=prec)
+    psi = (torch.randn(nx, ny, nz, dtype=propagator.PRECISIONS[prec], device="cuda") * 1e-3).contiguous()
     P = _lib
     passes = [("Z_MID", P.PASS_Z_MID, 40), ("Y_FWD", P.PASS_Y_FWD, 32), ("X_KIN", P.PASS_X_KIN, 32),
               ("Y_INV", P.PASS_Y_INV, 32), ("Z_FIRST", P.PASS_Z_FIRST, 40), ("Z_LAST", P.PASS_Z_LAST, 40),
               ("Z_FWD", P.PASS_Z_FWD, 32), ("X_FWD", P.PASS_X_FWD, 32), ("X_INV", P.PASS_X_INV, 32)]
     kbuf = torch.empty_like(psi)
     passes += [("Y_COPY", 60, 32), ("X_COPY", 61, 32)]
-    passes += [("Y_FWD_BLK", P.PASS_Y_FWD_BLK, 32), ("X_KIN_BLK", P.PASS_X_KIN_BLK, 32),
-               ("Y_INV_BLK", P.PASS_Y_INV_BLK, 32)]
     io = {P.PASS_Y_FWD_BLK: (psi, kbuf), P.PASS_X_KIN_BLK: (kbuf, kbuf), P.PASS_Y_INV_BLK: (kbuf, psi)}
     total = 0.0
     for name, kind, bpp in passes:
@@ -48,7 +47,7 @@ def main():
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / reps
-        gbs = bpp * n / (ms * 1e-3) / 1e9
+        gbs = bpp * (0.5 if prec == "complex64" and bpp % 16 == 0 else 1.0) * n / (ms * 1e-3) / 1e9
         if name in ("Z_MID", "Y_FWD", "X_KIN", "Y_INV"):
             total += ms
         print(f"{name:8s} {ms:8.3f} ms  {gbs:8.1f} GB/s")

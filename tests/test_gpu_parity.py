@@ -179,3 +179,32 @@ def test_determinism_bitwise():
     a2, t2 = run()
     assert np.array_equal(a1, a2)
     assert np.array_equal(t1, t2)
+
+
+@pytest.mark.parametrize("steps", [300])
+def test_complex64_mode_within_1e4(steps):
+    """Optional complex64 mode (north_star): exact FP64 phases, complex64
+    storage and transforms, held to <= 1e-4 against the complex128 oracle."""
+    d = load_golden("ioffe_32x16x32.npz")
+    grid = product_grid(d)
+    psi = qgrid.Wavefunction(d["psi0"].copy(), grid)
+    plan = propagator.make_plan(grid, d["V"], float(d["mass"]), float(d["dt"]), precision="complex64")
+    rec = observables.PopulationRecorder(partition_of(d, grid), stride=int(d["stride"]))
+    psi, _ = propagator.evolve_real(psi, plan, steps, [rec])
+    got = psi.amplitudes
+    assert got.dtype == np.complex64
+    assert rel_l2(got.astype(np.complex128), d["psi"]) <= 1e-4
+    assert np.abs(rec.trace.as_array()[:, 1:4] - d["trace"][:, 1:4]).max() <= 1e-4
+
+
+def test_complex64_fft_and_reductions():
+    rng = np.random.default_rng(4)
+    n = (16, 64, 32)
+    a = (rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(np.complex64)
+    grid = qgrid.SimGrid(n, (1e-5,) * 3, (0.0,) * 3)
+    plan = propagator._aux_plan(grid, torch.complex64)
+    d = torch.from_numpy(a.copy()).cuda()
+    plan.fft3d(d, -1)
+    assert rel_l2(d.cpu().numpy(), np.fft.fftn(a.astype(np.complex128))) <= 1e-6
+    w = qgrid.Wavefunction(a.copy(), grid)
+    assert w.norm() == pytest.approx(float(np.sum(np.abs(a.astype(np.complex128)) ** 2) * grid.dvol), rel=1e-6)

@@ -141,3 +141,9 @@ def test_symmetric_partition():
     part = obs.symmetric_partition(g, 3.5e-6)
     assert part.xb1.shape == (32,) and np.all(part.xb1 == -3.5e-6) and np.all(part.xb2 == 3.5e-6)
     assert not part.merged.any() and part.grid_ref is g
+
+
+def test_unknown_precision_rejected():
+    g = qgrid.make_grid(8, 8, 8, (1e-5,) * 3)
+    with pytest.raises((ValueError, RuntimeError)):
+        prop.make_plan(g, np.zeros(g.n), M, 1e-6, precision="complex32")
