@@ -167,10 +167,10 @@ struct SmemContig {
   C* base;
   __device__ __forceinline__ C& at(int i) const { return base[pad8(i)]; }
 };
-template <typename C>
-struct SmemStrided {  // column-fastest tile: element i of column c at i*8 + c
+template <typename C, int W = 8>
+struct SmemStrided {  // column-fastest tile of W columns: element i of column c at i*W + c
   C* base;            // points at column c
-  __device__ __forceinline__ C& at(int i) const { return base[i * 8]; }
+  __device__ __forceinline__ C& at(int i) const { return base[i * W]; }
 };
 
 // Barrier among the threads that share one exchange buffer.

@@ -30,6 +30,7 @@ enum PassKind {
   // diagnostics: the strided passes' memory traffic without the transforms
   PASS_Y_COPY = 60,
   PASS_X_COPY = 61,
+  PASS_XB_COPY = 62,
   // strided kernel variants
   PASS_S_FWD = 100,
   PASS_S_INV = 101,

@@ -34,8 +34,12 @@
 #ifndef CTAP_OCC
 #define CTAP_OCC 1024
 #endif
+// z columns per x-pass tile (8 or 16)
+#ifndef CTAP_XW
+#define CTAP_XW 8
+#endif
 #ifndef CTAP_Z_MINB
-#define CTAP_Z_MINB 4
+#define CTAP_Z_MINB 3
 #endif
 #ifndef CTAP_Z_MINB_TAB
 #define CTAP_Z_MINB_TAB 2
@@ -191,14 +195,14 @@ __global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::
 #define CTAP_TILE_E 8
 #endif
 
-template <int L, typename CV>
+template <int L, typename CV, int W>
 struct TileCfg {
   static constexpr int E = (L >= 256) ? CTAP_TILE_E : kElems;
   static constexpr int T = L / E;
-  static constexpr int per_tile = T * 8;
+  static constexpr int per_tile = T * W;
   static constexpr int G = per_tile >= 128 ? 1 : 128 / per_tile;  // tiles per block
   static constexpr int threads = G * per_tile;
-  static constexpr size_t smem = (size_t)G * L * 8 * sizeof(CV);
+  static constexpr size_t smem = (size_t)G * L * W * sizeof(CV);
   static constexpr int occ = CTAP_OCC * kElems / E;  // same register file, E/8 x the registers
   static constexpr int minb = occ / threads > 0 ? occ / threads : 1;
   static constexpr int minb_tab = CTAP_OCC_TAB / threads > 0 ? CTAP_OCC_TAB / threads : 1;
@@ -234,9 +238,9 @@ struct TileArgs {
   PhaseArgs ph;
 };
 
-template <int L, int E, int KIND, bool KTAB, bool KBLK, typename CV>
+template <int L, int E, int KIND, bool KTAB, bool KBLK, typename CV, int W>
 __device__ __forceinline__ void tile_body(const TileArgs& a, CV* v, int t, uint32_t o, uint32_t z,
-                                          bool active, const CV* __restrict__ tw, SmemStrided<CV> sm) {
+                                          bool active, const CV* __restrict__ tw, SmemStrided<CV, W> sm) {
   constexpr int T = L / E;
   if constexpr (KIND == T_COPY) {  // diagnostics: the pass's memory traffic without the transform
   } else if constexpr (KIND == T_FWD) {
@@ -273,27 +277,28 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, CV* v, int t, uint3
   }
 }
 
-template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV>
-__global__ void __launch_bounds__(TileCfg<L, CV>::threads, KTAB ? TileCfg<L, CV>::minb_tab : TileCfg<L, CV>::minb)
+template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W>
+__global__ void __launch_bounds__(TileCfg<L, CV, W>::threads,
+                                  KTAB ? TileCfg<L, CV, W>::minb_tab : TileCfg<L, CV, W>::minb)
     tile_kernel(TileArgs a, const CV* __restrict__ tw) {
-  using Cfg = TileCfg<L, CV>;
+  using Cfg = TileCfg<L, CV, W>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CV* smem = reinterpret_cast<CV*>(smem_raw);
   const CV* in = (const CV*)a.in;
   CV* out = (CV*)a.out;
-  const int col = threadIdx.x & 7;
-  const int t = (threadIdx.x >> 3) % Cfg::T;
+  const int col = threadIdx.x & (W - 1);
+  const int t = (threadIdx.x / W) % Cfg::T;
   const int g = threadIdx.x / Cfg::per_tile;
   const uint32_t tile = blockIdx.x * Cfg::G + g;
   const bool active = tile < a.n_outer * a.nchunk;
   const uint32_t o = active ? tile / a.nchunk : 0;
-  const uint32_t z = (active ? (tile - o * a.nchunk) : 0) * 8 + col;
+  const uint32_t z = (active ? (tile - o * a.nchunk) : 0) * W + col;
   constexpr int E = Cfg::E;
   const uint32_t obi = outer(a.lin, o) + z, obo = outer(a.lout, o) + z;
   CV v[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = active ? in[obi + inner<PIN>(a.lin, t + m * Cfg::T)] : CT<CV>::mk(0, 0);
-  tile_body<L, E, KIND, KTAB, POUT>(a, v, t, o, z, active, tw, SmemStrided<CV>{smem + (size_t)g * L * 8 + col});
+  tile_body<L, E, KIND, KTAB, POUT>(a, v, t, o, z, active, tw, SmemStrided<CV, W>{smem + (size_t)g * L * W + col});
   if (active) {
 #pragma unroll
     for (int m = 0; m < E; ++m) out[obo + inner<POUT>(a.lout, t + m * Cfg::T)] = v[m];
@@ -320,10 +325,10 @@ static cudaError_t launch_z(const ZArgs& a, const CV* tw, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV>
+template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W>
 static cudaError_t launch_tile(const TileArgs& a, const CV* tw, cudaStream_t st) {
-  using Cfg = TileCfg<L, CV>;
-  auto k = tile_kernel<L, KIND, PIN, POUT, KTAB, CV>;
+  using Cfg = TileCfg<L, CV, W>;
+  auto k = tile_kernel<L, KIND, PIN, POUT, KTAB, CV, W>;
   static cudaError_t init = allow_smem(k, Cfg::smem);
   if (init != cudaSuccess) return init;
   const uint32_t ntiles = a.n_outer * a.nchunk;
@@ -357,11 +362,11 @@ static cudaError_t dispatch_z(int L, bool c64, const ZArgs& a, Tw tw, cudaStream
 #undef CTAP_Z
 }
 
-template <int KIND, bool PIN, bool POUT, bool KTAB>
+template <int KIND, bool PIN, bool POUT, bool KTAB, int W = 8>
 static cudaError_t dispatch_tile(int L, bool c64, const TileArgs& a, Tw tw, cudaStream_t st) {
 #define CTAP_T(LL)                                                             \
-  (c64 ? launch_tile<LL, KIND, PIN, POUT, KTAB, float2>(a, tw.f, st)           \
-       : launch_tile<LL, KIND, PIN, POUT, KTAB, double2>(a, tw.d, st))
+  (c64 ? launch_tile<LL, KIND, PIN, POUT, KTAB, float2, W>(a, tw.f, st)        \
+       : launch_tile<LL, KIND, PIN, POUT, KTAB, double2, W>(a, tw.d, st))
   CTAP_BY_LENGTH(L, CTAP_T)
 #undef CTAP_T
 }
@@ -489,6 +494,8 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
   const int64_t nx = p->n[0], ny = p->n[1], nz = p->n[2];
   const bool c64 = p->dtype == CTAP_C64;
   const Tw tw_any = twid(p, 8);
+  // x passes read 16-column (instead of 8) tiles when z allows it
+  const bool xw16 = CTAP_XW == 16 && nz >= 16;
   const int P = p->slab_p;
   const uint32_t nxl = (uint32_t)(nx / P), nyl = (uint32_t)(ny / P);
   PhaseArgs ph;
@@ -597,7 +604,20 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       a.n_outer = nyl;
       a.lin = x_nat;
       a.lout = x_nat;
+      if (xw16) {
+        a.nchunk = (uint32_t)(nz / 16);
+        return dispatch_tile<T_COPY, false, false, false, 16>((int)nx, c64, a, tw_any, st);
+      }
       return dispatch_tile<T_COPY, false, false, false>((int)nx, c64, a, tw_any, st);
+    case PASS_XB_COPY: {  // diagnostics: x-pass traffic on the x-blocked layout, block 16
+      const int dlx = 4;
+      const uint32_t DL = 1u << dlx;
+      const Layout xb{DL * NZ, NY * DL * NZ, NZ, dlx, 0u, kNone};
+      a.n_outer = NY;
+      a.lin = xb;
+      a.lout = xb;
+      return dispatch_tile<T_COPY, true, true, false>((int)nx, c64, a, tw_any, st);
+    }
     case PASS_X_KIN:
     case PASS_X_FWD:
     case PASS_X_INV: {
@@ -607,6 +627,14 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       a.ph.outer_off = (uint32_t)p->slab_r * nyl;
       const Tw tw = twid(p, nx);
       const int L = (int)nx;
+      if (xw16) {  // 16-column tiles: 256-byte rows for the large-stride x lines
+        a.nchunk = (uint32_t)(nz / 16);
+        if (kind == PASS_X_KIN)
+          return p->expk_dev && p->k_lx == 0 ? dispatch_tile<T_KIN, false, false, true, 16>(L, c64, a, tw, st)
+                                             : dispatch_tile<T_KIN, false, false, false, 16>(L, c64, a, tw, st);
+        if (kind == PASS_X_FWD) return dispatch_tile<T_FWD, false, false, false, 16>(L, c64, a, tw, st);
+        return dispatch_tile<T_INV, false, false, false, 16>(L, c64, a, tw, st);
+      }
       if (kind == PASS_X_KIN)
         return p->expk_dev && p->k_lx == 0 ? dispatch_tile<T_KIN, false, false, true>(L, c64, a, tw, st)
                                            : dispatch_tile<T_KIN, false, false, false>(L, c64, a, tw, st);

@@ -41,7 +41,7 @@ PRECISIONS = {"complex128": torch.complex128, "complex64": torch.complex64}
 # measurements
 PHASE_TABLE_V = 1
 PHASE_TABLE_K = 2
-DEFAULT_PHASE_TABLES = int(os.environ.get("CTAP_PHASE_TABLES", str(PHASE_TABLE_V)))
+DEFAULT_PHASE_TABLES = int(os.environ.get("CTAP_PHASE_TABLES", "0"))
 
 
 class ConvergenceError(RuntimeError):

@@ -25,14 +25,14 @@ def main():
     v = torch.full((nx, ny, nz), muB / 2 * 0.03, dtype=torch.float64, device="cuda")
     v += torch.rand_like(v) * 1e-29
     prec = os.environ.get('CTAP_PRECISION', 'complex128')
-    plan = propagator.make_plan(grid, v, m, 1e-6, phase_tables=int(os.environ.get('CTAP_PHASE_TABLES', '1')), precision=prec)
+    plan = propagator.make_plan(grid, v, m, 1e-6, phase_tables=int(os.environ.get('CTAP_PHASE_TABLES', '0')), precision=prec)
     psi = (torch.randn(nx, ny, nz, dtype=propagator.PRECISIONS[prec], device="cuda") * 1e-3).contiguous()
     P = _lib
     passes = [("Z_MID", P.PASS_Z_MID, 40), ("Y_FWD", P.PASS_Y_FWD, 32), ("X_KIN", P.PASS_X_KIN, 32),
               ("Y_INV", P.PASS_Y_INV, 32), ("Z_FIRST", P.PASS_Z_FIRST, 40), ("Z_LAST", P.PASS_Z_LAST, 40),
               ("Z_FWD", P.PASS_Z_FWD, 32), ("X_FWD", P.PASS_X_FWD, 32), ("X_INV", P.PASS_X_INV, 32)]
     kbuf = torch.empty_like(psi)
-    passes += [("Y_COPY", 60, 32), ("X_COPY", 61, 32)]
+    passes += [("Y_COPY", 60, 32), ("X_COPY", 61, 32), ("XB_COPY", 62, 32)]
     io = {P.PASS_Y_FWD_BLK: (psi, kbuf), P.PASS_X_KIN_BLK: (kbuf, kbuf), P.PASS_Y_INV_BLK: (kbuf, psi)}
     total = 0.0
     for name, kind, bpp in passes:
