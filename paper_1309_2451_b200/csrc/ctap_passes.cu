@@ -24,15 +24,20 @@
 // same values (16 B/pt for the full V step and for K, no sincos per step);
 // both give bit-identical phases.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "ctap_device.cuh"
 #include "ctap_internal.h"
+#include "ctap_tile.cuh"
 
 // resident threads per SM the register allocation of the strided kernels is
 // sized for, and min blocks per SM of the z kernels (256 threads)
 #ifndef CTAP_OCC
 #define CTAP_OCC 1024
+#endif
+#ifndef CTAP_TMA_DEFAULT
+#define CTAP_TMA_DEFAULT 1
 #endif
 // z columns per x-pass tile (8 or 16)
 #ifndef CTAP_XW
@@ -49,53 +54,6 @@
 #endif
 
 namespace ctap {
-
-enum TileKind { T_FWD, T_INV, T_KIN, T_VFIRST, T_VMID, T_VLAST, T_COPY };
-
-struct PhaseArgs {
-  const double* vi;     // v_i = (V - shift)/E0 at the element offsets of psi (z passes)
-  const void* expv;     // exp(-i v_i dt_i) table, complex of the plan's precision (VTAB)
-  const double* kx2;    // k^2 along the pass axis (x pass)
-  const double* ky2;    // k^2 along the outer axis, global
-  const double* kz2;    // k^2 along z
-  const void* expk;     // exp(-i k^2 dt/2)/N table in the x-pass layout (KTAB)
-  uint32_t outer_off;   // global index of outer o = 0
-  double len2, dt_i;
-  double scale;         // folded inverse normalisation 1/N (power of two)
-  int imag;             // imaginary time: real decay factors
-};
-
-// v *= exp(i coef v_i dt) (real time) or exp(coef v_i dt) (imaginary time)
-// (the phase and its cos/sin are always evaluated in FP64; complex64 mode
-// rounds the factor to float)
-template <typename CV>
-__device__ __forceinline__ void mul_vphase(CV& v, double vi, double coef, const PhaseArgs& a) {
-  using R = typename CT<CV>::R;
-  const double phi = v_phase_i(vi, coef, a.dt_i);
-  if (a.imag) {
-    const R f = (R)exp(phi);
-    v = CT<CV>::mk(v.x * f, v.y * f);
-  } else {
-    double s, c;
-    fast_sincos(phi, &s, &c);
-    v = cmul(v, CT<CV>::mk((R)c, (R)s));
-  }
-}
-
-// v *= exp(-i k^2 dt/2) / N at (kx2, ky2, kz2)
-template <typename CV>
-__device__ __forceinline__ void mul_kphase(CV& v, double kx2, double ky2, double kz2, const PhaseArgs& a) {
-  using R = typename CT<CV>::R;
-  const double phi = k_phase(kx2, ky2, kz2, a.len2, a.dt_i);
-  if (a.imag) {
-    const R f = (R)(exp(phi) * a.scale);
-    v = CT<CV>::mk(v.x * f, v.y * f);
-  } else {
-    double s, c;
-    fast_sincos(phi, &s, &c);
-    v = cmul(v, CT<CV>::mk((R)(c * a.scale), (R)(s * a.scale)));
-  }
-}
 
 // ---------------------------------------------------------------------------
 // z passes
@@ -207,75 +165,6 @@ struct TileCfg {
   static constexpr int minb = occ / threads > 0 ? occ / threads : 1;
   static constexpr int minb_tab = CTAP_OCC_TAB / threads > 0 ? CTAP_OCC_TAB / threads : 1;
 };
-
-// Element (o, i, z) of a strided tile lives at outer(o) + inner(i) + z:
-//   outer(o) = (o >> olb)*osb + (o & (2^olb - 1))*so      (olb = 31: o*so)
-//   inner(i) = i*si                                       (plain)
-//            = (i >> lb)*sb + (i & (2^lb - 1))*si          (blocked: the slab
-//              transpose buffers and the blocked k-space layout)
-struct Layout {
-  uint32_t so, sb, si;
-  int lb;
-  uint32_t osb;
-  int olb;
-};
-
-__device__ __forceinline__ uint32_t outer(const Layout& l, uint32_t o) {
-  return (o >> l.olb) * l.osb + (o & ((1u << l.olb) - 1u)) * l.so;
-}
-template <bool BLK>
-__device__ __forceinline__ uint32_t inner(const Layout& l, uint32_t i) {
-  if constexpr (BLK) return (i >> l.lb) * l.sb + (i & ((1u << l.lb) - 1u)) * l.si;
-  else return i * l.si;
-}
-
-struct TileArgs {
-  const void* in;
-  void* out;
-  Layout lin, lout;
-  uint32_t n_outer;  // number of outer indices
-  uint32_t nchunk;   // 8-column chunks per outer index (nz / 8)
-  PhaseArgs ph;
-};
-
-template <int L, int E, int KIND, bool KTAB, bool KBLK, typename CV, int W>
-__device__ __forceinline__ void tile_body(const TileArgs& a, CV* v, int t, uint32_t o, uint32_t z,
-                                          bool active, const CV* __restrict__ tw, SmemStrided<CV, W> sm) {
-  constexpr int T = L / E;
-  if constexpr (KIND == T_COPY) {  // diagnostics: the pass's memory traffic without the transform
-  } else if constexpr (KIND == T_FWD) {
-    line_fft<L, -1, E>(v, t, tw, sm, SyncBlock{});
-  } else if constexpr (KIND == T_INV) {
-    line_fft<L, +1, E>(v, t, tw, sm, SyncBlock{});
-  } else {  // T_KIN: forward, K/N, inverse
-    // operands of the phase, loaded ahead of the forward transform so their
-    // latency hides behind it
-    double kx2[E], ky2 = 0.0, kz2 = 0.0;
-    CV f[E];
-    if constexpr (KTAB) {
-      const CV* expk = (const CV*)a.ph.expk;
-#pragma unroll
-      for (int m = 0; m < E; ++m)
-        f[m] = active ? __ldcg(&expk[outer(a.lout, o) + inner<KBLK>(a.lout, t + m * T) + z]) : CT<CV>::mk(0, 0);
-    } else {
-      ky2 = __ldg(&a.ph.ky2[a.ph.outer_off + o]);
-      kz2 = __ldg(&a.ph.kz2[z]);
-#pragma unroll
-      for (int m = 0; m < E; ++m) kx2[m] = __ldg(&a.ph.kx2[t + m * T]);
-    }
-    line_fft<L, -1, E>(v, t, tw, sm, SyncBlock{});
-    if (active) {
-      if constexpr (KTAB) {
-#pragma unroll
-        for (int m = 0; m < E; ++m) v[m] = cmul(v[m], f[m]);
-      } else {
-#pragma unroll
-        for (int m = 0; m < E; ++m) mul_kphase(v[m], kx2[m], ky2, kz2, a.ph);
-      }
-    }
-    line_fft<L, +1, E>(v, t, tw, sm, SyncBlock{});
-  }
-}
 
 template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W>
 __global__ void __launch_bounds__(TileCfg<L, CV, W>::threads,
@@ -485,6 +374,9 @@ cudaError_t ctap_run_phase_table(const ctap_plan* p, int which, void* out, cudaS
 
 // Run one pass on the plan's local data.  `in`/`out` may alias (natural
 // layouts, in place).  Returns a CUDA error code.
+cudaError_t ctap_run_tma_pass(const ctap_plan* p, int axis, int kind, void* data, const TileArgs& a,
+                              cudaStream_t st);
+
 static Tw twid(const ctap_plan* p, int64_t L) {
   const int off = p->tw_off[ilog2(L) - 3];
   return Tw{p->twiddles + off, p->twiddles32 + off};
@@ -496,6 +388,15 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
   const Tw tw_any = twid(p, 8);
   // x passes read 16-column (instead of 8) tiles when z allows it
   const bool xw16 = CTAP_XW == 16 && nz >= 16;
+  // strided passes on natural layouts go through the TMA pipeline
+  // (y passes in complex64; x passes only on request: a single TMA-fed CTA
+  // per SM loses to two register-fed CTAs there)
+  static const int tma_mode = [] {
+    const char* e = getenv("CTAP_TMA");
+    return e ? atoi(e) : CTAP_TMA_DEFAULT;
+  }();
+  const bool use_tma = tma_mode != 0;
+  const bool use_tma_x = tma_mode == 2;
   const int P = p->slab_p;
   const uint32_t nxl = (uint32_t)(nx / P), nyl = (uint32_t)(ny / P);
   PhaseArgs ph;
@@ -592,6 +493,10 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       a.lin = y_nat;
       a.lout = y_nat;
       const bool fwd = (kind == PASS_Y_FWD || kind == PASS_Y_FWD_TO_PEER);
+      if (use_tma && c64 && in == out) {  // measured: faster for complex64 only
+        cudaError_t e = ctap_run_tma_pass(p, 1, fwd ? T_FWD : T_INV, out, a, st);
+        if (e != cudaErrorNotSupported) return e;
+      }
       return fwd ? dispatch_tile<T_FWD, false, false, false>(L, c64, a, tw, st)
                  : dispatch_tile<T_INV, false, false, false>(L, c64, a, tw, st);
     }
@@ -627,6 +532,11 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       a.ph.outer_off = (uint32_t)p->slab_r * nyl;
       const Tw tw = twid(p, nx);
       const int L = (int)nx;
+      if (use_tma_x && in == out && !(kind == PASS_X_KIN && p->expk_dev)) {
+        const int tk = kind == PASS_X_KIN ? T_KIN : kind == PASS_X_FWD ? T_FWD : T_INV;
+        cudaError_t e = ctap_run_tma_pass(p, 2, tk, out, a, st);
+        if (e != cudaErrorNotSupported) return e;
+      }
       if (xw16) {  // 16-column tiles: 256-byte rows for the large-stride x lines
         a.nchunk = (uint32_t)(nz / 16);
         if (kind == PASS_X_KIN)

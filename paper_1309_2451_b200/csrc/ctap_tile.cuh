@@ -1,0 +1,128 @@
+// Shared pieces of the axis-pass kernels: pass kinds, phase arguments and
+// the exact phase multiplies, strided-tile layouts and the tile transform
+// body (used by tile_kernel in ctap_passes.cu and tma_tile_kernel in
+// ctap_tma.cu).
+#pragma once
+
+#include "ctap_device.cuh"
+
+namespace ctap {
+
+enum TileKind { T_FWD, T_INV, T_KIN, T_VFIRST, T_VMID, T_VLAST, T_COPY };
+
+struct PhaseArgs {
+  const double* vi;     // v_i = (V - shift)/E0 at the element offsets of psi (z passes)
+  const void* expv;     // exp(-i v_i dt_i) table, complex of the plan's precision (VTAB)
+  const double* kx2;    // k^2 along the pass axis (x pass)
+  const double* ky2;    // k^2 along the outer axis, global
+  const double* kz2;    // k^2 along z
+  const void* expk;     // exp(-i k^2 dt/2)/N table in the x-pass layout (KTAB)
+  uint32_t outer_off;   // global index of outer o = 0
+  double len2, dt_i;
+  double scale;         // folded inverse normalisation 1/N (power of two)
+  int imag;             // imaginary time: real decay factors
+};
+
+// v *= exp(i coef v_i dt) (real time) or exp(coef v_i dt) (imaginary time)
+// (the phase and its cos/sin are always evaluated in FP64; complex64 mode
+// rounds the factor to float)
+template <typename CV>
+__device__ __forceinline__ void mul_vphase(CV& v, double vi, double coef, const PhaseArgs& a) {
+  using R = typename CT<CV>::R;
+  const double phi = v_phase_i(vi, coef, a.dt_i);
+  if (a.imag) {
+    const R f = (R)exp(phi);
+    v = CT<CV>::mk(v.x * f, v.y * f);
+  } else {
+    double s, c;
+    fast_sincos(phi, &s, &c);
+    v = cmul(v, CT<CV>::mk((R)c, (R)s));
+  }
+}
+
+// v *= exp(-i k^2 dt/2) / N at (kx2, ky2, kz2)
+template <typename CV>
+__device__ __forceinline__ void mul_kphase(CV& v, double kx2, double ky2, double kz2, const PhaseArgs& a) {
+  using R = typename CT<CV>::R;
+  const double phi = k_phase(kx2, ky2, kz2, a.len2, a.dt_i);
+  if (a.imag) {
+    const R f = (R)(exp(phi) * a.scale);
+    v = CT<CV>::mk(v.x * f, v.y * f);
+  } else {
+    double s, c;
+    fast_sincos(phi, &s, &c);
+    v = cmul(v, CT<CV>::mk((R)(c * a.scale), (R)(s * a.scale)));
+  }
+}
+
+// Element (o, i, z) of a strided tile lives at outer(o) + inner(i) + z:
+//   outer(o) = (o >> olb)*osb + (o & (2^olb - 1))*so      (olb = 31: o*so)
+//   inner(i) = i*si                                       (plain)
+//            = (i >> lb)*sb + (i & (2^lb - 1))*si          (blocked: the slab
+//              transpose buffers and the blocked k-space layout)
+struct Layout {
+  uint32_t so, sb, si;
+  int lb;
+  uint32_t osb;
+  int olb;
+};
+
+__device__ __forceinline__ uint32_t outer(const Layout& l, uint32_t o) {
+  return (o >> l.olb) * l.osb + (o & ((1u << l.olb) - 1u)) * l.so;
+}
+template <bool BLK>
+__device__ __forceinline__ uint32_t inner(const Layout& l, uint32_t i) {
+  if constexpr (BLK) return (i >> l.lb) * l.sb + (i & ((1u << l.lb) - 1u)) * l.si;
+  else return i * l.si;
+}
+
+struct TileArgs {
+  const void* in;
+  void* out;
+  Layout lin, lout;
+  uint32_t n_outer;  // number of outer indices
+  uint32_t nchunk;   // 8-column chunks per outer index (nz / 8)
+  PhaseArgs ph;
+};
+
+template <int L, int E, int KIND, bool KTAB, bool KBLK, typename CV, int W>
+__device__ __forceinline__ void tile_body(const TileArgs& a, CV* v, int t, uint32_t o, uint32_t z,
+                                          bool active, const CV* __restrict__ tw, SmemStrided<CV, W> sm) {
+  constexpr int T = L / E;
+  if constexpr (KIND == T_COPY) {  // diagnostics: the pass's memory traffic without the transform
+  } else if constexpr (KIND == T_FWD) {
+    line_fft<L, -1, E>(v, t, tw, sm, SyncBlock{});
+  } else if constexpr (KIND == T_INV) {
+    line_fft<L, +1, E>(v, t, tw, sm, SyncBlock{});
+  } else {  // T_KIN: forward, K/N, inverse
+    // operands of the phase, loaded ahead of the forward transform so their
+    // latency hides behind it
+    double kx2[E], ky2 = 0.0, kz2 = 0.0;
+    CV f[E];
+    if constexpr (KTAB) {
+      const CV* expk = (const CV*)a.ph.expk;
+#pragma unroll
+      for (int m = 0; m < E; ++m)
+        f[m] = active ? __ldcg(&expk[outer(a.lout, o) + inner<KBLK>(a.lout, t + m * T) + z]) : CT<CV>::mk(0, 0);
+    } else {
+      ky2 = __ldg(&a.ph.ky2[a.ph.outer_off + o]);
+      kz2 = __ldg(&a.ph.kz2[z]);
+#pragma unroll
+      for (int m = 0; m < E; ++m) kx2[m] = __ldg(&a.ph.kx2[t + m * T]);
+    }
+    line_fft<L, -1, E>(v, t, tw, sm, SyncBlock{});
+    if (active) {
+      if constexpr (KTAB) {
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = cmul(v[m], f[m]);
+      } else {
+#pragma unroll
+        for (int m = 0; m < E; ++m) mul_kphase(v[m], kx2[m], ky2, kz2, a.ph);
+      }
+    }
+    line_fft<L, +1, E>(v, t, tw, sm, SyncBlock{});
+  }
+}
+
+
+}  // namespace ctap
