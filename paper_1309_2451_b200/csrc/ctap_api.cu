@@ -41,6 +41,15 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 bool pow2_in_range(int64_t n) { return n >= 8 && n <= 1024 && (n & (n - 1)) == 0; }
 
+constexpr int kGraphSteps = 16;
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CTAP_GRAPHS");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
 }  // namespace
 
 #define CUDA_TRY(expr, what)                       \
@@ -148,6 +157,8 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
   cudaFree(p->expv_dev);
   cudaFree(p->expk_dev);
   cudaFree(p->kbuf);
+  if (p->g_exec) cudaGraphExecDestroy(p->g_exec);
+  if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   delete p;
   return CTAP_OK;
 }
@@ -175,7 +186,37 @@ CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
   if (n == 0) return CTAP_OK;
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Z_FIRST, psi, psi, st), "ctap_advance");
-  for (int64_t j = 0; j < n; ++j) {
+  // interior steps in CUDA-graph chunks: one launch per kGraphSteps steps
+  // instead of 4 (removes the per-kernel launch cost that dominates small grids)
+  int64_t j = 0;
+  if (graphs_enabled() && !p->kbuf && n - 1 >= kGraphSteps) {
+    if (p->g_exec == nullptr || p->g_psi != psi || p->g_steps != kGraphSteps) {
+      if (p->g_exec) cudaGraphExecDestroy(p->g_exec);
+      p->g_exec = nullptr;
+      if (!p->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking), "ctap_advance");
+      cudaGraph_t g = nullptr;
+      CUDA_TRY(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal), "ctap_advance capture");
+      cudaError_t ce = cudaSuccess;
+      for (int m = 0; m < kGraphSteps && ce == cudaSuccess; ++m) {
+        ce = ctap_run_pass(p, CTAP_PASS_Y_FWD, psi, psi, p->cap_stream);
+        if (ce == cudaSuccess) ce = ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, p->cap_stream);
+        if (ce == cudaSuccess) ce = ctap_run_pass(p, CTAP_PASS_Y_INV, psi, psi, p->cap_stream);
+        if (ce == cudaSuccess) ce = ctap_run_pass(p, CTAP_PASS_Z_MID, psi, psi, p->cap_stream);
+      }
+      cudaError_t ee = cudaStreamEndCapture(p->cap_stream, &g);
+      if (ce == cudaSuccess) ce = ee;
+      if (ce == cudaSuccess) ce = cudaGraphInstantiate(&p->g_exec, g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (ce != cudaSuccess) {
+        p->g_exec = nullptr;
+        return cuda_fail(ce, "ctap_advance graph capture");
+      }
+      p->g_psi = psi;
+      p->g_steps = kGraphSteps;
+    }
+    for (; j + kGraphSteps <= n - 1; j += kGraphSteps) CUDA_TRY(cudaGraphLaunch(p->g_exec, st), "ctap_advance");
+  }
+  for (; j < n; ++j) {
     if (p->kbuf) {
       CUDA_TRY(ctap_run_pass(p, ctap::PASS_Y_FWD_BLK, psi, p->kbuf, st), "ctap_advance");
       CUDA_TRY(ctap_run_pass(p, ctap::PASS_X_KIN_BLK, p->kbuf, p->kbuf, st), "ctap_advance");

@@ -57,6 +57,12 @@ struct ctap_plan {
   double2* kbuf;           // single-GPU k-space buffer (blocked layout, out of place y passes)
   int k_lx;                // log2 of the x block of the k-space layout (0: natural)
   double* red_partial;     // reduction scratch
+  // CUDA graph of M interior steps (launch-bound small grids), captured on a
+  // private stream for one psi pointer and replayed on the caller's stream
+  cudaStream_t cap_stream;
+  cudaGraphExec_t g_exec;
+  const void* g_psi;
+  int g_steps;
   int red_blocks;
 };
 

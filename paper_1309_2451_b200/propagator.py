@@ -444,7 +444,10 @@ class AsyncSnapshotObserver:
         self.out_dir = out_dir
         self.stride = stride
         self.written = []
-        self._q = queue.Queue(maxsize=2)
+        self._q = queue.Queue()
+        self._free = queue.Queue()  # indices of snapshot buffers not in flight
+        for i in range(3):
+            self._free.put(i)
         self._bufs = {}
         self._stream = None
         self._err = None
@@ -456,13 +459,15 @@ class AsyncSnapshotObserver:
             item = self._q.get()
             if item is None:
                 return
-            path, event, host, grid, t = item
+            path, event, host, grid, t, idx = item
             try:
                 event.synchronize()
                 write_snapshot(path, host.numpy(), grid, time=t)
                 self.written.append(path)
             except BaseException as exc:  # surfaced by close()
                 self._err = exc
+            finally:
+                self._free.put(idx)  # the buffer pair may be refilled now
 
     def notify(self, step_index: int, psi):
         import os
@@ -474,9 +479,8 @@ class AsyncSnapshotObserver:
         if key not in self._bufs:
             self._bufs[key] = [(torch.empty_like(d), torch.empty(d.shape, dtype=d.dtype, pin_memory=True))
                                for _ in range(3)]
-            self._next = 0
-        dev_buf, host = self._bufs[key][self._next % 3]
-        self._next += 1
+        idx = self._free.get()  # blocks while all three snapshots are still in flight
+        dev_buf, host = self._bufs[key][idx]
         dev_buf.copy_(d)                                # on the propagation stream
         ready = torch.cuda.Event()
         ready.record()
@@ -486,7 +490,7 @@ class AsyncSnapshotObserver:
             done = torch.cuda.Event()
             done.record(self._stream)
         path = os.path.join(str(self.out_dir), f"psi_{step_index:07d}.qwf")
-        self._q.put((path, done, host, psi.grid, psi.time))
+        self._q.put((path, done, host, psi.grid, psi.time, idx))
 
     def close(self):
         self._q.put(None)

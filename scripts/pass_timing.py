@@ -53,7 +53,7 @@ def main():
         print(f"{name:8s} {ms:8.3f} ms  {gbs:8.1f} GB/s")
     # full steps
     for _ in range(2):
-        plan.native.advance(psi, 5)
+        plan.native.advance(psi, reps)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     s.record()
