@@ -163,7 +163,8 @@ def run_ours(args):
     amp0 = (torch.from_numpy(fx)[:, None, None] * torch.from_numpy(fy)[None, :, None]
             * torch.from_numpy(fz)[None, None, :]).to(torch.complex128)
     psi = amp0.to(dev).contiguous()
-    prop = slab.SlabPropagator(grid, v_local, m, DT, phase_tables=args.phase_tables)
+    prop = slab.SlabPropagator(grid, v_local, m, DT, phase_tables=args.phase_tables,
+                               transport=args.transport)
     tables = prop.phase_tables
 
     def barrier():
@@ -204,9 +205,13 @@ def run_ours(args):
 
     # per-pass device times (CUDA events, same stream) -> dominant kernel roofline
     nloc = lay.points
-    bufs = {"psi": psi.reshape(-1), "send": prop.send, "recv": prop.recv}
+    if world > 1 and prop.transport == "fused":
+        bufs = {"psi": psi.reshape(-1), "send": psi.reshape(-1), "recv": psi.reshape(-1)}
+    else:
+        bufs = {"psi": psi.reshape(-1), "send": prop.send, "recv": prop.recv}
     vtab = 16 if tables & propagator.PHASE_TABLE_V else 8
     ktab = 16 if tables & propagator.PHASE_TABLE_K else 0
+    fused = world > 1 and prop.transport == "fused"
     passes = [("z_mid [z^-1 V z]", _lib.PASS_Z_MID, "psi", "psi", 32 + vtab),
               ("y_fwd", _lib.PASS_Y_FWD_TO_PEER if world > 1 else _lib.PASS_Y_FWD, "psi",
                "send" if world > 1 else "psi", 32),
@@ -216,6 +221,8 @@ def run_ours(args):
                "send" if world > 1 else "psi", "psi", 32)]
     per_pass = {}
     reps = max(3, min(20, args.steps))
+    if fused:  # the fused passes need the plan-owned exchange buffers
+        passes = [("z_mid [z^-1 V z]", _lib.PASS_Z_MID, "psi", "psi", 32 + vtab)]
     for name, kind, src, dst, bpp in passes:
         for _ in range(2):
             prop.native.run_pass(kind, bufs[src], bufs[dst])
@@ -409,6 +416,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--phase-tables", type=int, default=None,
                     help="mask: 1 = exp(-iV dt) table, 2 = exp(-ik^2dt/2) table (default: library default)")
+    ap.add_argument("--transport", choices=["fused", "nccl"], default="fused",
+                    help="slab transposes: fused NVLink peer stores (default) or NCCL all-to-all")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)

@@ -70,7 +70,14 @@ typedef enum ctap_pass_kind {
    * B(x, y, z) = ((x >> lx) ny + y) 2^lx nz + (x & (2^lx - 1)) nz + z */
   CTAP_PASS_Y_FWD_BLK = 12,  /* y FFT, natural psi -> blocked buffer */
   CTAP_PASS_X_KIN_BLK = 13,  /* [x K x^-1] on the blocked buffer, in place */
-  CTAP_PASS_Y_INV_BLK = 14   /* y^-1, blocked buffer -> natural psi */
+  CTAP_PASS_Y_INV_BLK = 14,  /* y^-1, blocked buffer -> natural psi */
+  /* slab decomposition with the transposes fused into the passes (no NCCL
+   * all-to-all): the output goes straight into the other ranks' buffers
+   * (peer memory over NVLink) registered with ctap_set_peer_buffers; the
+   * caller inserts a stream-ordered cross-rank barrier after each. */
+  CTAP_PASS_Y_FWD_TO_PEERS = 15, /* in: psi x-slab; out: every rank's y-slab buffer */
+  CTAP_PASS_X_KIN_TO_PEERS = 16  /* in: this rank's y-slab buffer; out: every rank's
+                                    peer-major buffer (then CTAP_PASS_Y_INV_FROM_PEER) */
 } ctap_pass_kind;
 
 typedef struct ctap_plan ctap_plan;
@@ -143,6 +150,21 @@ CTAP_API int ctap_density_xz(ctap_plan* plan, const void* psi_dev, double* out_d
  * ctap_v_sums: on position space, out_dev[2] = [ sum V |psi|^2, sum |psi|^2 ]. */
 CTAP_API int ctap_k2_sums(ctap_plan* plan, const void* phi_dev, double* out_dev, void* stream);
 CTAP_API int ctap_v_sums(ctap_plan* plan, const void* psi_dev, double* out_dev, void* stream);
+
+/* Register, for the fused slab passes, the device addresses (as seen by this
+ * process: peer-mapped through ctap_ipc_open, or local) of every rank's
+ * buffers: which = 0: the y-slab buffers (nx, ny/P, nz) the y pass writes;
+ * which = 1: the peer-major buffers [P][nx/P][ny/P][nz] the x pass writes.
+ * count must equal slab_p (<= 16). */
+CTAP_API int ctap_set_peer_buffers(ctap_plan* plan, int32_t which, void* const* ptrs, int32_t count);
+
+/* CUDA IPC helpers for the peer mapping: export a device allocation made by
+ * cudaMalloc (64-byte handle), open a peer's handle, close it. */
+CTAP_API int ctap_ipc_handle(void* dev_ptr, void* handle64);
+CTAP_API int ctap_ipc_open(const void* handle64, void** dev_ptr);
+CTAP_API int ctap_ipc_close(void* dev_ptr);
+CTAP_API int ctap_device_alloc(int64_t bytes, void** dev_ptr);
+CTAP_API int ctap_device_free(void* dev_ptr);
 
 /* StepPlan.exp_v_half / exp_v_full / exp_k (propagator.py:45-47, 65-68,
  * 76-78) materialised on the local slab for inspection (which = 0, 1, 2):

@@ -30,12 +30,15 @@ PASS_Z_FWD, PASS_Z_INV, PASS_Z_FIRST, PASS_Z_MID, PASS_Z_LAST = range(5)
 PASS_Y_FWD, PASS_Y_INV, PASS_Y_FWD_TO_PEER, PASS_Y_INV_FROM_PEER = range(5, 9)
 PASS_X_KIN, PASS_X_FWD, PASS_X_INV = range(9, 12)
 PASS_Y_FWD_BLK, PASS_X_KIN_BLK, PASS_Y_INV_BLK = range(12, 15)
+PASS_Y_FWD_TO_PEERS, PASS_X_KIN_TO_PEERS = 15, 16
 
 # every symbol include/ctap.h declares
 EXPORTS = (
     "ctap_plan_create", "ctap_plan_destroy", "ctap_advance", "ctap_pass", "ctap_observe",
     "ctap_density_xz", "ctap_k2_sums", "ctap_v_sums", "ctap_phase_field", "ctap_scale",
     "ctap_fft3d", "ctap_potential", "ctap_last_error", "ctap_version",
+    "ctap_set_peer_buffers", "ctap_ipc_handle", "ctap_ipc_open", "ctap_ipc_close",
+    "ctap_device_alloc", "ctap_device_free",
 )
 
 
@@ -86,6 +89,12 @@ def load():
         "ctap_scale": [p, p, d, p],
         "ctap_fft3d": [p, p, i32, p],
         "ctap_potential": [p, i64, p, i64, p, i64, p, p, p, i64, d, d, d, d, d, d, d, d, p, p],
+        "ctap_set_peer_buffers": [p, i32, ctypes.POINTER(p), i32],
+        "ctap_ipc_handle": [p, p],
+        "ctap_ipc_open": [p, ctypes.POINTER(p)],
+        "ctap_ipc_close": [p],
+        "ctap_device_alloc": [i64, ctypes.POINTER(p)],
+        "ctap_device_free": [p],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

@@ -166,11 +166,16 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
 CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, void* stream) {
   if (!p || !in || !out) return fail(CTAP_EINVAL, "null argument");
   const bool diag = kind == ctap::PASS_Y_COPY || kind == ctap::PASS_X_COPY || kind == ctap::PASS_XB_COPY;
-  if (!diag && (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_Y_INV_BLK))
+  if (!diag && (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_X_KIN_TO_PEERS))
     return fail(CTAP_EINVAL, "unknown pass %d", kind);
   const bool blk = kind >= CTAP_PASS_Y_FWD_BLK && kind <= CTAP_PASS_Y_INV_BLK;
   if (blk && p->slab_p != 1) return fail(CTAP_EINVAL, "blocked k-space passes are single-GPU");
   if (blk && in == out && kind != CTAP_PASS_X_KIN_BLK) return fail(CTAP_EINVAL, "blocked y passes run out of place");
+  if (kind == CTAP_PASS_Y_FWD_TO_PEERS || kind == CTAP_PASS_X_KIN_TO_PEERS) {
+    void* const* tab = kind == CTAP_PASS_Y_FWD_TO_PEERS ? p->peer_y : p->peer_p;
+    for (int q = 0; q < p->slab_p; ++q)
+      if (!tab[q]) return fail(CTAP_EINVAL, "peer buffers not registered (ctap_set_peer_buffers)");
+  }
   if (kind <= CTAP_PASS_Z_LAST && in != out) return fail(CTAP_EINVAL, "z passes run in place");
   if ((kind == CTAP_PASS_Z_FIRST || kind == CTAP_PASS_Z_MID || kind == CTAP_PASS_Z_LAST) && !p->vi_dev)
     return fail(CTAP_EINVAL, "plan has no potential");
@@ -272,6 +277,51 @@ CTAP_API int ctap_v_sums(ctap_plan* p, const void* psi, double* out, void* strea
   if (!p || !psi || !out) return fail(CTAP_EINVAL, "null argument");
   if (!p->v_dev) return fail(CTAP_EINVAL, "plan has no potential");
   CUDA_TRY(ctap_run_v_sums(p, psi, out, (cudaStream_t)stream), "ctap_v_sums");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_set_peer_buffers(ctap_plan* p, int32_t which, void* const* ptrs, int32_t count) {
+  if (!p || !ptrs) return fail(CTAP_EINVAL, "null argument");
+  if (which != 0 && which != 1) return fail(CTAP_EINVAL, "which must be 0 (y-slab) or 1 (peer-major)");
+  if (count != p->slab_p || count > 16) return fail(CTAP_EINVAL, "expected %d peer buffers", p->slab_p);
+  void** tab = which == 0 ? p->peer_y : p->peer_p;
+  for (int q = 0; q < count; ++q) {
+    if (!ptrs[q]) return fail(CTAP_EINVAL, "peer buffer %d is null", q);
+    tab[q] = ptrs[q];
+  }
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_ipc_handle(void* dev_ptr, void* handle64) {
+  if (!dev_ptr || !handle64) return fail(CTAP_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, dev_ptr), "ctap_ipc_handle");
+  std::memcpy(handle64, &h, sizeof h);
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail(CTAP_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "ctap_ipc_open");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(CTAP_EINVAL, "null argument");
+  CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr), "ctap_ipc_close");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_device_alloc(int64_t bytes, void** dev_ptr) {
+  if (!dev_ptr || bytes <= 0) return fail(CTAP_EINVAL, "bad allocation request");
+  CUDA_TRY(cudaMalloc(dev_ptr, (size_t)bytes), "ctap_device_alloc");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_device_free(void* dev_ptr) {
+  CUDA_TRY(cudaFree(dev_ptr), "ctap_device_free");
   return CTAP_OK;
 }
 

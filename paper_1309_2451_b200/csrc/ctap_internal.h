@@ -27,6 +27,8 @@ enum PassKind {
   PASS_Y_FWD_BLK = CTAP_PASS_Y_FWD_BLK,  // y FFT, natural -> blocked k-space buffer
   PASS_X_KIN_BLK = CTAP_PASS_X_KIN_BLK,  // [x K x^-1] on the blocked buffer, in place
   PASS_Y_INV_BLK = CTAP_PASS_Y_INV_BLK,  // y^-1, blocked buffer -> natural
+  PASS_Y_FWD_TO_PEERS = CTAP_PASS_Y_FWD_TO_PEERS,
+  PASS_X_KIN_TO_PEERS = CTAP_PASS_X_KIN_TO_PEERS,
   // diagnostics: the strided passes' memory traffic without the transforms
   PASS_Y_COPY = 60,
   PASS_X_COPY = 61,
@@ -56,6 +58,8 @@ struct ctap_plan {
   int tw_off[8];           // start of the table of L = 8 << i
   double2* kbuf;           // single-GPU k-space buffer (blocked layout, out of place y passes)
   int k_lx;                // log2 of the x block of the k-space layout (0: natural)
+  void* peer_y[16];        // fused slab transposes: every rank's y-slab buffer
+  void* peer_p[16];        // and peer-major buffer (peer-mapped device addresses)
   double* red_partial;     // reduction scratch
   // CUDA graph of M interior steps (launch-bound small grids), captured on a
   // private stream for one psi pointer and replayed on the caller's stream

@@ -166,7 +166,7 @@ struct TileCfg {
   static constexpr int minb_tab = CTAP_OCC_TAB / threads > 0 ? CTAP_OCC_TAB / threads : 1;
 };
 
-template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W>
+template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W, bool PEERS = false>
 __global__ void __launch_bounds__(TileCfg<L, CV, W>::threads,
                                   KTAB ? TileCfg<L, CV, W>::minb_tab : TileCfg<L, CV, W>::minb)
     tile_kernel(TileArgs a, const CV* __restrict__ tw) {
@@ -189,8 +189,22 @@ __global__ void __launch_bounds__(TileCfg<L, CV, W>::threads,
   for (int m = 0; m < E; ++m) v[m] = active ? in[obi + inner<PIN>(a.lin, t + m * Cfg::T)] : CT<CV>::mk(0, 0);
   tile_body<L, E, KIND, KTAB, POUT>(a, v, t, o, z, active, tw, SmemStrided<CV, W>{smem + (size_t)g * L * W + col});
   if (active) {
+    if constexpr (PEERS) {
+      // fused transpose: each point goes straight into the owning rank's
+      // buffer (peer memory over NVLink); the fence makes the stores visible
+      // before the stream-ordered cross-rank barrier that follows the kernel
+      const uint32_t mask = (1u << a.lout.lb) - 1u;
 #pragma unroll
-    for (int m = 0; m < E; ++m) out[obo + inner<POUT>(a.lout, t + m * Cfg::T)] = v[m];
+      for (int m = 0; m < E; ++m) {
+        const uint32_t i = t + m * Cfg::T;
+        CV* dst = (CV*)a.peers[i >> a.lout.lb];
+        dst[obo + (i & mask) * a.lout.si] = v[m];
+      }
+      __threadfence_system();
+    } else {
+#pragma unroll
+      for (int m = 0; m < E; ++m) out[obo + inner<POUT>(a.lout, t + m * Cfg::T)] = v[m];
+    }
   }
 }
 
@@ -214,10 +228,10 @@ static cudaError_t launch_z(const ZArgs& a, const CV* tw, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W>
+template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W, bool PEERS = false>
 static cudaError_t launch_tile(const TileArgs& a, const CV* tw, cudaStream_t st) {
   using Cfg = TileCfg<L, CV, W>;
-  auto k = tile_kernel<L, KIND, PIN, POUT, KTAB, CV, W>;
+  auto k = tile_kernel<L, KIND, PIN, POUT, KTAB, CV, W, PEERS>;
   static cudaError_t init = allow_smem(k, Cfg::smem);
   if (init != cudaSuccess) return init;
   const uint32_t ntiles = a.n_outer * a.nchunk;
@@ -251,11 +265,11 @@ static cudaError_t dispatch_z(int L, bool c64, const ZArgs& a, Tw tw, cudaStream
 #undef CTAP_Z
 }
 
-template <int KIND, bool PIN, bool POUT, bool KTAB, int W = 8>
+template <int KIND, bool PIN, bool POUT, bool KTAB, int W = 8, bool PEERS = false>
 static cudaError_t dispatch_tile(int L, bool c64, const TileArgs& a, Tw tw, cudaStream_t st) {
-#define CTAP_T(LL)                                                             \
-  (c64 ? launch_tile<LL, KIND, PIN, POUT, KTAB, float2, W>(a, tw.f, st)        \
-       : launch_tile<LL, KIND, PIN, POUT, KTAB, double2, W>(a, tw.d, st))
+#define CTAP_T(LL)                                                                   \
+  (c64 ? launch_tile<LL, KIND, PIN, POUT, KTAB, float2, W, PEERS>(a, tw.f, st)       \
+       : launch_tile<LL, KIND, PIN, POUT, KTAB, double2, W, PEERS>(a, tw.d, st))
   CTAP_BY_LENGTH(L, CTAP_T)
 #undef CTAP_T
 }
@@ -385,6 +399,7 @@ static Tw twid(const ctap_plan* p, int64_t L) {
 cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* out, cudaStream_t st) {
   const int64_t nx = p->n[0], ny = p->n[1], nz = p->n[2];
   const bool c64 = p->dtype == CTAP_C64;
+  const size_t csz = c64 ? sizeof(float2) : sizeof(double2);
   const Tw tw_any = twid(p, 8);
   // x passes read 16-column (instead of 8) tiles when z allows it
   const bool xw16 = CTAP_XW == 16 && nz >= 16;
@@ -452,6 +467,27 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
   const Layout x_blk{XL * NZ, NY * XL * NZ, NZ, lx, 0u, kNone};  // x-pass view
   const bool peer = P > 1;
   switch (kind) {
+    case PASS_Y_FWD_TO_PEERS: {
+      // y FFT of the x-slab; point (x_local, y, z) lands in rank q = y / ny_local
+      // at ((r nx_local + x_local) ny_local + y % ny_local) nz + z
+      a.n_outer = nxl;
+      a.lin = y_nat;
+      a.lout = Layout{nyl * NZ, 0u, NZ, ilog2(nyl), 0u, kNone};
+      for (int q = 0; q < P; ++q)
+        a.peers[q] = (char*)p->peer_y[q] + csz * (size_t)p->slab_r * nxl * nyl * NZ;
+      return dispatch_tile<T_FWD, false, true, false, 8, true>((int)ny, c64, a, twid(p, ny), st);
+    }
+    case PASS_X_KIN_TO_PEERS: {
+      // [x K x^-1] of the y-slab; point (x, y_local, z) lands in rank q = x / nx_local
+      // at r (nx_local ny_local nz) + (x % nx_local) ny_local nz + y_local nz + z
+      a.n_outer = nyl;
+      a.lin = x_nat;
+      a.lout = Layout{NZ, 0u, nyl * NZ, ilog2(nxl), 0u, kNone};
+      a.ph.outer_off = (uint32_t)p->slab_r * nyl;
+      for (int q = 0; q < P; ++q)
+        a.peers[q] = (char*)p->peer_p[q] + csz * (size_t)p->slab_r * nxl * nyl * NZ;
+      return dispatch_tile<T_KIN, false, true, false, 8, true>((int)nx, c64, a, twid(p, nx), st);
+    }
     case PASS_Y_FWD_BLK:
     case PASS_Y_INV_BLK: {
       a.n_outer = nxl;

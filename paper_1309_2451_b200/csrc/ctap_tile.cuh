@@ -76,6 +76,8 @@ __device__ __forceinline__ uint32_t inner(const Layout& l, uint32_t i) {
   else return i * l.si;
 }
 
+constexpr int kMaxRanks = 16;
+
 struct TileArgs {
   const void* in;
   void* out;
@@ -83,6 +85,9 @@ struct TileArgs {
   uint32_t n_outer;  // number of outer indices
   uint32_t nchunk;   // 8-column chunks per outer index (nz / 8)
   PhaseArgs ph;
+  // fused slab transpose: destination of inner block b (= rank b) is peers[b]
+  // (a peer GPU's buffer, mapped over NVLink, base offset included)
+  void* peers[kMaxRanks];
 };
 
 template <int L, int E, int KIND, bool KTAB, bool KBLK, typename CV, int W>

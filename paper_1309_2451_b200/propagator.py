@@ -98,6 +98,14 @@ class NativePlan:
         _lib.call("ctap_pass", self.handle, int(kind), src.data_ptr(), dst.data_ptr(),
                   _device.stream_handle())
 
+    def run_pass_ptr(self, kind: int, src: int, dst: int):
+        """A pass on raw device addresses (plan-external buffers)."""
+        _lib.call("ctap_pass", self.handle, int(kind), src, dst, _device.stream_handle())
+
+    def set_peer_buffers(self, which: int, ptrs):
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        _lib.call("ctap_set_peer_buffers", self.handle, int(which), arr, len(ptrs))
+
     def fft3d(self, data: torch.Tensor, direction: int = -1):
         _lib.call("ctap_fft3d", self.handle, data.data_ptr(), int(direction), _device.stream_handle())
 

@@ -15,13 +15,20 @@ receive buffer of the first all-to-all is already the natural y-slab layout
 the x pass runs on.  Observer sums are per-rank partials combined in rank
 order on every rank (deterministic, no float atomics).
 
-The schedule (SlabSchedule) is independent of the compute backend so the
-same code drives the CUDA passes here and the CPU emulation in the gloo
-tests (tests/test_slab_gloo.py).
+Two transports: "nccl" (the y/x passes write the all-to-all buffers, NCCL
+all_to_all_single moves them) and "fused" (the y pass and the x pass store
+their outputs directly into the other ranks' buffers through CUDA-IPC peer
+mappings over NVLink, so the transpose rides inside the pass's own HBM write
+and there is no separate all-to-all sweep; a stream-ordered barrier follows
+each).  The schedules are independent of the compute backend, so the same
+code drives the CUDA passes here, the virtual-rank GPU tests and the CPU
+emulation in the gloo tests (tests/test_slab_gloo.py).
 """
 
 from __future__ import annotations
 
+import ctypes
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -98,6 +105,46 @@ def segment_schedule(n_steps: int):
         yield ("pass", _lib.PASS_Z_MID if j < n_steps - 1 else _lib.PASS_Z_LAST, "psi", "psi")
 
 
+def segment_schedule_fused(n_steps: int):
+    """The same n merged steps with the transposes fused into the passes:
+    the y pass stores its output straight into every rank's y-slab buffer and
+    the x pass into every rank's peer-major buffer (NVLink peer stores), each
+    followed by a stream-ordered cross-rank barrier.  Ops: ('pass', kind, src,
+    dst) and ('barrier',)."""
+    if n_steps <= 0:
+        return
+    yield ("pass", _lib.PASS_Z_FIRST, "psi", "psi")
+    for j in range(n_steps):
+        yield ("pass", _lib.PASS_Y_FWD_TO_PEERS, "psi", "psi")
+        yield ("barrier",)
+        yield ("pass", _lib.PASS_X_KIN_TO_PEERS, "yslab", "yslab")
+        yield ("barrier",)
+        yield ("pass", _lib.PASS_Y_INV_FROM_PEER, "peer", "psi")
+        yield ("pass", _lib.PASS_Z_MID if j < n_steps - 1 else _lib.PASS_Z_LAST, "psi", "psi")
+
+
+class DeviceBuffer:
+    """cudaMalloc'd buffer owned by libctap (exportable through CUDA IPC)."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = int(nbytes)
+        h = ctypes.c_void_p()
+        _lib.call("ctap_device_alloc", self.nbytes, ctypes.byref(h))
+        self.ptr = int(h.value)
+        self._fin = weakref.finalize(self, _lib.load().ctap_device_free, ctypes.c_void_p(self.ptr))
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _lib.call("ctap_ipc_handle", ctypes.c_void_p(self.ptr), buf)
+        return buf.raw
+
+
+def open_ipc(handle: bytes) -> int:
+    h = ctypes.c_void_p()
+    _lib.call("ctap_ipc_open", ctypes.create_string_buffer(handle, 64), ctypes.byref(h))
+    return int(h.value)
+
+
 def combine_in_rank_order(local: torch.Tensor, group=None) -> torch.Tensor:
     """Sum per-rank partial sums in rank order (bitwise identical on every rank)."""
     P = dist.get_world_size(group)
@@ -113,7 +160,8 @@ class SlabPropagator:
     """Real- or imaginary-time propagation of one rank's x-slab on its GPU."""
 
     def __init__(self, grid, v_local, mass: float, dt: float, group=None, mode: str = REAL_TIME,
-                 v_shift: float = 0.0, phase_tables: int | None = None, precision: str = "complex128"):
+                 v_shift: float = 0.0, phase_tables: int | None = None, precision: str = "complex128",
+                 transport: str = "nccl"):
         self.grid = as_simgrid(grid)
         self.group = group
         P = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -131,8 +179,44 @@ class SlabPropagator:
                                  slab_p=P, slab_r=r, phase_tables=phase_tables, precision=precision)
         dev = self.v_local.device
         dt_ = self.native.torch_dtype
-        self.send = torch.empty(self.layout.points, dtype=dt_, device=dev)
-        self.recv = torch.empty(self.layout.points, dtype=dt_, device=dev)
+        if transport not in ("nccl", "fused"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport if P > 1 else "nccl"
+        if self.transport == "nccl":
+            self.send = torch.empty(self.layout.points, dtype=dt_, device=dev)
+            self.recv = torch.empty(self.layout.points, dtype=dt_, device=dev)
+        else:
+            self._setup_fused(dt_)
+
+    def _setup_fused(self, dtype):
+        """Allocate this rank's y-slab and peer-major buffers, exchange CUDA IPC
+        handles with every rank and register the peer-mapped addresses."""
+        itemsize = 8 if dtype == torch.complex64 else 16
+        nbytes = self.layout.points * itemsize
+        self.yslab = DeviceBuffer(nbytes)
+        self.peer = DeviceBuffer(nbytes)
+        mine = (self.yslab.ipc_handle(), self.peer.ipc_handle())
+        handles = [None] * self.layout.P
+        dist.all_gather_object(handles, mine, group=self.group)
+        self._opened = []
+        tabs = ([], [])
+        for q, (hy, hp) in enumerate(handles):
+            if q == self.layout.rank:
+                tabs[0].append(self.yslab.ptr)
+                tabs[1].append(self.peer.ptr)
+            else:
+                py, pp = open_ipc(hy), open_ipc(hp)
+                self._opened += [py, pp]
+                tabs[0].append(py)
+                tabs[1].append(pp)
+        self.native.set_peer_buffers(0, tabs[0])
+        self.native.set_peer_buffers(1, tabs[1])
+        self._flag = torch.zeros(1, dtype=torch.float32, device=self.v_local.device)
+
+    def _barrier(self):
+        # stream-ordered: every rank's preceding pass (and its system fence)
+        # completes before any rank's next pass starts
+        dist.all_reduce(self._flag, group=self.group)
 
     def _a2a(self, src: torch.Tensor, dst: torch.Tensor):
         if self.layout.P == 1:
@@ -146,6 +230,14 @@ class SlabPropagator:
             raise ValueError("n_steps must be >= 0")
         if self.layout.P == 1:
             self.native.advance(psi_local, n_steps)
+            return
+        if self.transport == "fused":
+            addr = {"psi": psi_local.data_ptr(), "yslab": self.yslab.ptr, "peer": self.peer.ptr}
+            for op in segment_schedule_fused(n_steps):
+                if op[0] == "pass":
+                    self.native.run_pass_ptr(op[1], addr[op[2]], addr[op[3]])
+                else:
+                    self._barrier()
             return
         bufs = {"psi": psi_local.reshape(-1), "send": self.send, "recv": self.recv}
         for op in segment_schedule(n_steps):

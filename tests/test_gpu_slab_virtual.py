@@ -104,3 +104,51 @@ def test_yslab_kinetic_sums_compose():
         tot = [tot[0] + s[0], tot[1] + s[1]]
     assert tot[0] == pytest.approx(ref[0], rel=1e-13)
     assert tot[1] == pytest.approx(ref[1], rel=1e-13)
+
+
+def run_virtual_fused(grid, v, a0, P, steps, tables=0):
+    """The fused transport on one GPU: each virtual rank's y and x passes
+    store directly into the other ranks' buffers through the peer tables
+    (device addresses on the same GPU instead of NVLink peer mappings)."""
+    from paper_1309_2451_b200.slab import segment_schedule_fused
+
+    lays = [SlabLayout(grid.n, P, r) for r in range(P)]
+    vs = [torch.from_numpy(np.ascontiguousarray(v[l.x_slice])).cuda() for l in lays]
+    plans = [NativePlan(grid, vs[r], M, 1e-6, slab_p=P, slab_r=r, phase_tables=tables) for r in range(P)]
+    psi = [torch.from_numpy(np.ascontiguousarray(a0[l.x_slice])).cuda().reshape(-1) for l in lays]
+    yslab = [torch.empty(l.points, dtype=torch.complex128, device="cuda") for l in lays]
+    peer = [torch.empty(l.points, dtype=torch.complex128, device="cuda") for l in lays]
+    for pl in plans:
+        pl.set_peer_buffers(0, [b.data_ptr() for b in yslab])
+        pl.set_peer_buffers(1, [b.data_ptr() for b in peer])
+    for op in segment_schedule_fused(steps):
+        if op[0] == "barrier":
+            continue  # ranks run one after another: every store has landed
+        for r in range(P):
+            bufs = {"psi": psi[r], "yslab": yslab[r], "peer": peer[r]}
+            plans[r].run_pass(op[1], bufs[op[2]], bufs[op[3]])
+    return torch.cat(psi).reshape(grid.n).cpu().numpy()
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_fused_transport_bitwise_equal_single_gpu(P):
+    grid, v, a0 = _case()
+    got = run_virtual_fused(grid, v, a0, P, 6)
+    psi = qgrid.Wavefunction(a0.copy(), grid)
+    plan = propagator.make_plan(grid, v, M, 1e-6, phase_tables=0)
+    psi, _ = propagator.evolve_real(psi, plan, 6)
+    assert np.array_equal(got, psi.amplitudes)
+
+
+def test_fused_pass_requires_registered_peers():
+    grid, v, a0 = _case()
+    pl = NativePlan(grid, torch.from_numpy(np.ascontiguousarray(v[:16])).cuda(), M, 1e-6, slab_p=2, slab_r=0)
+    x = torch.zeros(16 * 16 * 32, dtype=torch.complex128, device="cuda")
+    with pytest.raises(ValueError, match="peer buffers not registered"):
+        pl.run_pass(_lib_pass("PASS_Y_FWD_TO_PEERS"), x, x)
+
+
+def _lib_pass(name):
+    from paper_1309_2451_b200 import _lib
+
+    return getattr(_lib, name)

@@ -117,3 +117,17 @@ def test_schedule_shape():
     assert ops[-1] == ("pass", _lib.PASS_Z_LAST, "psi", "psi")
     assert sum(1 for o in ops if o[0] == "a2a") == 6
     assert sum(1 for o in ops if o[0] == "pass" and o[1] == _lib.PASS_Z_MID) == 2
+
+
+def test_fused_schedule_shape():
+    from paper_1309_2451_b200 import _lib
+    from paper_1309_2451_b200.slab import segment_schedule_fused
+
+    assert list(segment_schedule_fused(0)) == []
+    ops = list(segment_schedule_fused(2))
+    kinds = [o[1] if o[0] == "pass" else "barrier" for o in ops]
+    assert kinds == [_lib.PASS_Z_FIRST,
+                     _lib.PASS_Y_FWD_TO_PEERS, "barrier", _lib.PASS_X_KIN_TO_PEERS, "barrier",
+                     _lib.PASS_Y_INV_FROM_PEER, _lib.PASS_Z_MID,
+                     _lib.PASS_Y_FWD_TO_PEERS, "barrier", _lib.PASS_X_KIN_TO_PEERS, "barrier",
+                     _lib.PASS_Y_INV_FROM_PEER, _lib.PASS_Z_LAST]
