@@ -161,9 +161,10 @@ class SlabPropagator:
 
     def __init__(self, grid, v_local, mass: float, dt: float, group=None, mode: str = REAL_TIME,
                  v_shift: float = 0.0, phase_tables: int | None = None, precision: str = "complex128",
-                 transport: str = "nccl"):
+                 transport: str = "nccl", barrier=None):
         self.grid = as_simgrid(grid)
         self.group = group
+        self._barrier_fn = barrier  # fused transport: default is a 1-float NCCL all-reduce
         P = dist.get_world_size(group) if dist.is_initialized() else 1
         r = dist.get_rank(group) if dist.is_initialized() else 0
         self.layout = SlabLayout(tuple(self.grid.n), P, r)
@@ -216,7 +217,10 @@ class SlabPropagator:
     def _barrier(self):
         # stream-ordered: every rank's preceding pass (and its system fence)
         # completes before any rank's next pass starts
-        dist.all_reduce(self._flag, group=self.group)
+        if self._barrier_fn is not None:
+            self._barrier_fn()
+        else:
+            dist.all_reduce(self._flag, group=self.group)
 
     def _a2a(self, src: torch.Tensor, dst: torch.Tensor):
         if self.layout.P == 1:
