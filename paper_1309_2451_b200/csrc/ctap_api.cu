@@ -58,6 +58,33 @@ bool graphs_enabled() {
     if (e_ != cudaSuccess) return cuda_fail(e_, what); \
   } while (0)
 
+// Find val with fl(fl(2 pi * fl(m val))^2) == k2[i] for every index i
+// (m = i for i < n/2, i - n otherwise), searching a few ulps around the
+// estimate from k2[1].  Host arithmetic is plain IEEE double (no contraction
+// in this translation unit's host code for these products).
+static bool recover_kval(const double* k2, int64_t n, double* val) {
+  if (n < 2 || !(k2[1] > 0.0)) return false;
+  const double twopi = 6.283185307179586;
+  volatile double est = std::sqrt(k2[1]) / twopi;
+  double c = est;
+  for (int step = 0; step < 8; ++step) c = std::nextafter(c, 0.0);
+  for (int tries = 0; tries < 17; ++tries, c = std::nextafter(c, 1e300)) {
+    bool ok = true;
+    for (int64_t i = 0; i < n && ok; ++i) {
+      const int64_t m = i < n / 2 ? i : i - n;
+      volatile double mv = (double)m * c;
+      volatile double k = twopi * mv;
+      volatile double kk = k * k;
+      ok = kk == k2[i];
+    }
+    if (ok) {
+      *val = c;
+      return true;
+    }
+  }
+  return false;
+}
+
 extern "C" {
 
 CTAP_API const char* ctap_last_error(void) { return g_err.c_str(); }
@@ -99,6 +126,11 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
     e = cudaMalloc((void**)&p->k2_dev[i], sizeof(double) * d->n[i]);
     if (e == cudaSuccess) e = cudaMemcpy(p->k2_dev[i], k2h[i], sizeof(double) * d->n[i], cudaMemcpyHostToDevice);
   }
+  // the x pass regenerates k^2 in registers when the tables are numpy's
+  // (2 pi * fftfreq(n, d))^2 for some val = 1/(n d), checked bit for bit
+  p->kgen = 1;
+  for (int i = 0; i < 3; ++i) p->kgen &= recover_kval(k2h[i], d->n[i], &p->kval[i]);
+  if (const char* env = getenv("CTAP_KGEN")) p->kgen &= atoi(env) != 0;
   std::vector<double> tw = ctap_make_twiddles(p->tw_off);
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->twiddles, tw.size() * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(p->twiddles, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice);

@@ -52,6 +52,8 @@ struct ctap_plan {
   void* expv_dev;          // optional table exp(-i v_i dt_i), plan precision (phase_tables, real time)
   void* expk_dev;          // optional table exp(-i k^2 dt/2) / N, x-pass layout
   double* k2_dev[3];       // squared wavenumbers per axis (global lengths)
+  int kgen;                // k^2 regenerated on device from kval (tables verified)
+  double kval[3];          // 1/(n d) per axis (numpy fftfreq's val)
   int dtype;               // CTAP_C128 or CTAP_C64
   double2* twiddles;       // stage-major twiddle tables for L = 8..1024
   float2* twiddles32;      // the same, rounded to float (complex64 mode)

@@ -403,15 +403,17 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
   const Tw tw_any = twid(p, 8);
   // x passes read 16-column (instead of 8) tiles when z allows it
   const bool xw16 = CTAP_XW == 16 && nz >= 16;
-  // strided passes on natural layouts go through the TMA pipeline
-  // (y passes in complex64; x passes only on request: a single TMA-fed CTA
-  // per SM loses to two register-fed CTAs there)
+  // strided passes on natural layouts go through the TMA pipeline in
+  // complex64 (CTAP_TMA=1, default); in complex128 the register-fed
+  // tile_kernel measured faster (CTAP_TMA=2 adds c128 x, 3 c128 x and y;
+  // DESIGN.md §4)
   static const int tma_mode = [] {
     const char* e = getenv("CTAP_TMA");
     return e ? atoi(e) : CTAP_TMA_DEFAULT;
   }();
   const bool use_tma = tma_mode != 0;
-  const bool use_tma_x = tma_mode == 2;
+
+  const bool use_tma_x = tma_mode >= 2 || (tma_mode == 1 && c64);
   const int P = p->slab_p;
   const uint32_t nxl = (uint32_t)(nx / P), nyl = (uint32_t)(ny / P);
   PhaseArgs ph;
@@ -426,6 +428,11 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
   ph.scale = p->inv_scale;
   ph.imag = p->mode == 1;
   ph.outer_off = 0;
+  ph.kgen = p->kgen;
+  for (int i = 0; i < 3; ++i) {
+    ph.kn[i] = (uint32_t)p->n[i];
+    ph.kval[i] = p->kval[i];
+  }
 
   if (kind >= PASS_Z_FWD && kind <= PASS_Z_LAST) {
     if (in != out) return cudaErrorInvalidValue;
@@ -529,7 +536,7 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
       a.lin = y_nat;
       a.lout = y_nat;
       const bool fwd = (kind == PASS_Y_FWD || kind == PASS_Y_FWD_TO_PEER);
-      if (use_tma && c64 && in == out) {  // measured: faster for complex64 only
+      if (use_tma && (c64 || tma_mode == 3) && in == out) {  // measured: faster for complex64 only
         cudaError_t e = ctap_run_tma_pass(p, 1, fwd ? T_FWD : T_INV, out, a, st);
         if (e != cudaErrorNotSupported) return e;
       }

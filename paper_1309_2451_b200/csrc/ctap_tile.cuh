@@ -21,7 +21,21 @@ struct PhaseArgs {
   double len2, dt_i;
   double scale;         // folded inverse normalisation 1/N (power of two)
   int imag;             // imaginary time: real decay factors
+  // k^2 regenerated in registers instead of loaded (kgen != 0): the plan
+  // verified that (2 pi * (m * kval[a]))^2 reproduces every table entry
+  int kgen;
+  uint32_t kn[3];
+  double kval[3];
 };
+
+// squared angular wavenumber of FFT index i on an axis of n points with
+// 1/(n d) = val, formed as numpy's 2*pi*fftfreq(n, d) then squared
+// (qgrid.py k_axis / k_squared): ((2 pi) * (m * val))^2, m the signed index
+__device__ __forceinline__ double k2_gen(uint32_t i, uint32_t n, double val) {
+  const int m = i < (n >> 1) ? (int)i : (int)i - (int)n;
+  const double k = __dmul_rn(6.283185307179586, __dmul_rn((double)m, val));
+  return __dmul_rn(k, k);
+}
 
 // v *= exp(i coef v_i dt) (real time) or exp(coef v_i dt) (imaginary time)
 // (the phase and its cos/sin are always evaluated in FP64; complex64 mode
@@ -90,42 +104,48 @@ struct TileArgs {
   void* peers[kMaxRanks];
 };
 
-template <int L, int E, int KIND, bool KTAB, bool KBLK, typename CV, int W>
+template <int L, int E, int KIND, bool KTAB, bool KBLK, typename CV, int W, typename Sync = SyncBlock>
 __device__ __forceinline__ void tile_body(const TileArgs& a, CV* v, int t, uint32_t o, uint32_t z,
-                                          bool active, const CV* __restrict__ tw, SmemStrided<CV, W> sm) {
+                                          bool active, const CV* __restrict__ tw, SmemStrided<CV, W> sm,
+                                          Sync sync = Sync{}) {
   constexpr int T = L / E;
   if constexpr (KIND == T_COPY) {  // diagnostics: the pass's memory traffic without the transform
   } else if constexpr (KIND == T_FWD) {
-    line_fft<L, -1, E>(v, t, tw, sm, SyncBlock{});
+    line_fft<L, -1, E>(v, t, tw, sm, sync);
   } else if constexpr (KIND == T_INV) {
-    line_fft<L, +1, E>(v, t, tw, sm, SyncBlock{});
+    line_fft<L, +1, E>(v, t, tw, sm, sync);
   } else {  // T_KIN: forward, K/N, inverse
-    // operands of the phase, loaded ahead of the forward transform so their
-    // latency hides behind it
-    double kx2[E], ky2 = 0.0, kz2 = 0.0;
-    CV f[E];
+    // per-column operands ahead of the forward transform; the per-point kx^2
+    // after it (regenerated, or loaded), so no registers are held across it
+    double ky2 = 0.0, kz2 = 0.0;
+    CV f[KTAB ? E : 1];
     if constexpr (KTAB) {
       const CV* expk = (const CV*)a.ph.expk;
 #pragma unroll
       for (int m = 0; m < E; ++m)
         f[m] = active ? __ldcg(&expk[outer(a.lout, o) + inner<KBLK>(a.lout, t + m * T) + z]) : CT<CV>::mk(0, 0);
+    } else if (a.ph.kgen) {
+      ky2 = k2_gen(a.ph.outer_off + o, a.ph.kn[1], a.ph.kval[1]);
+      kz2 = k2_gen(z, a.ph.kn[2], a.ph.kval[2]);
     } else {
       ky2 = __ldg(&a.ph.ky2[a.ph.outer_off + o]);
       kz2 = __ldg(&a.ph.kz2[z]);
-#pragma unroll
-      for (int m = 0; m < E; ++m) kx2[m] = __ldg(&a.ph.kx2[t + m * T]);
     }
-    line_fft<L, -1, E>(v, t, tw, sm, SyncBlock{});
+    line_fft<L, -1, E>(v, t, tw, sm, sync);
     if (active) {
       if constexpr (KTAB) {
 #pragma unroll
         for (int m = 0; m < E; ++m) v[m] = cmul(v[m], f[m]);
+      } else if (a.ph.kgen) {
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+          mul_kphase(v[m], k2_gen(t + m * T, a.ph.kn[0], a.ph.kval[0]), ky2, kz2, a.ph);
       } else {
 #pragma unroll
-        for (int m = 0; m < E; ++m) mul_kphase(v[m], kx2[m], ky2, kz2, a.ph);
+        for (int m = 0; m < E; ++m) mul_kphase(v[m], __ldg(&a.ph.kx2[t + m * T]), ky2, kz2, a.ph);
       }
     }
-    line_fft<L, +1, E>(v, t, tw, sm, SyncBlock{});
+    line_fft<L, +1, E>(v, t, tw, sm, sync);
   }
 }
 

@@ -3,11 +3,11 @@
 // Same tile and thread mapping as tile_kernel (ctap_passes.cu): a tile is
 // 8 consecutive z columns x the whole line, thread (t, col) owns points
 // t + m*T of column col.  The difference is how the tile reaches the SM: a
-// persistent CTA per SM keeps two tile buffers in shared memory and one
-// elected thread streams the NEXT tile into the idle buffer with
-// cp.async.bulk.tensor (TMA, completion on an mbarrier) while all threads
-// transform the current one, so the HBM reads of tile k+1 overlap the
-// FP64 work of tile k instead of waiting behind it.  The landed buffer is the
+// persistent CTA per SM runs G independent compute groups (named barriers)
+// over NB > G tile buffers, and each group, when it releases a buffer, streams
+// a later tile into it with cp.async.bulk.tensor (TMA, completion on an
+// mbarrier).  HBM reads of the next tiles therefore overlap the FP64 work of
+// the current ones instead of waiting behind it.  The landed buffer is the
 // [i][8] tile in natural order, which doubles as the FFT exchange buffer.
 // Results go straight from registers to HBM (the stores do not stall).
 #include <cuda.h>
@@ -50,29 +50,53 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// Shared-memory pipeline of one persistent CTA: G compute groups of L
+// threads (8 columns x T = L/8 threads each) and NB > G tile buffers.  Local
+// tile j (global tile blockIdx.x + j*gridDim.x) lands in buffer j % NB and is
+// transformed by group j % G; when a group has finished a tile it streams tile
+// j + NB into the buffer it just released, so while each group computes, the
+// tiles of the next NB - G steps are already in flight.
+template <int L, typename CV>
+struct TmaCfg {
+  static constexpr int G = 1024 / L < 4 ? 1024 / L : 4;  // compute groups
+  static constexpr uint32_t kTileBytes = (uint32_t)L * 8 * sizeof(CV);
+  static constexpr int kMaxBuf = (int)((200u * 1024u) / kTileBytes);
+  static constexpr int NB = G + 2 <= kMaxBuf ? G + 2 : kMaxBuf;  // >= G + 1 required
+  static constexpr bool ok = NB >= G + 1;
+  static constexpr size_t smem = (size_t)NB * kTileBytes + 12 * NB;
+};
+
 // AXIS 1: y pass on (x, y, z) (o = x, line = y = tensor dim 1)
 // AXIS 2: x pass on (x, y, z) (o = y, line = x = tensor dim 2)
 template <int L, int KIND, typename CV, int AXIS>
-__global__ void __launch_bounds__(L, 1)
+__global__ void __launch_bounds__(L * TmaCfg<L, CV>::G, 1)
     tma_tile_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a, const CV* __restrict__ tw) {
+  using Cfg = TmaCfg<L, CV>;
   constexpr int E = kElems;
-  constexpr int T = L / E;  // threads per column; blockDim = 8 T = L
+  constexpr int T = L / E;  // threads per column; a group is 8 T = L threads
+  constexpr int G = Cfg::G, NB = Cfg::NB;
   constexpr int BOX = L < 256 ? L : 256;
-  constexpr uint32_t kTileBytes = (uint32_t)L * 8 * sizeof(CV);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  CV* buf0 = reinterpret_cast<CV*>(smem_raw);
-  CV* buf1 = buf0 + L * 8;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 2 * kTileBytes);
+  CV* bufs = reinterpret_cast<CV*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NB * Cfg::kTileBytes);
+  uint32_t* issued = reinterpret_cast<uint32_t*>(full + NB);  // fills issued per buffer - 1
   CV* out = (CV*)a.out;
-  const int col = threadIdx.x & 7;
-  const int t = threadIdx.x >> 3;
+  const int g = threadIdx.x / L;
+  const int lt = threadIdx.x - g * L;
+  const int col = lt & 7;
+  const int t = lt >> 3;
+  const SyncNamed gsync{1 + g, L};
   const uint32_t ntiles = a.n_outer * a.nchunk;
+  const uint32_t nloc = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-  auto issue = [&](uint32_t tile, CV* dst, uint64_t* bar) {
+  auto issue = [&](uint32_t j) {
+    const uint32_t tile = blockIdx.x + j * gridDim.x;
+    CV* dst = bufs + (size_t)(j % NB) * L * 8;
+    uint64_t* bar = &full[j % NB];
     const uint32_t o = tile / a.nchunk;
     const int c0 = (int)((tile - o * a.nchunk) * 8 * 2);  // in scalars (re, im)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bar, kTileBytes);
+    mbar_expect_tx(bar, Cfg::kTileBytes);
 #pragma unroll
     for (int b = 0; b < L / BOX; ++b) {
       if constexpr (AXIS == 1) tma_load_3d(dst + b * BOX * 8, &tmap, bar, c0, b * BOX, (int)o);
@@ -81,32 +105,45 @@ __global__ void __launch_bounds__(L, 1)
   };
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], 1);
+      issued[b] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x == 0 && blockIdx.x < ntiles) issue(blockIdx.x, buf0, &bars[0]);
+  if (threadIdx.x == 0)
+    for (uint32_t j = 0; j < (uint32_t)NB && j < nloc; ++j) issue(j);
 
-  uint32_t k = 0;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-    const int s = k & 1;
-    CV* cur = s ? buf1 : buf0;
-    // stream the next tile into the other buffer (freed by the barrier that
-    // ended the previous iteration) while this one is transformed
-    if (threadIdx.x == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, s ? buf0 : buf1, &bars[s ^ 1]);
-    mbar_wait(&bars[s], (k >> 1) & 1);
+  for (uint32_t j = g; j < nloc; j += G) {
+    const int b = j % NB;
+    const uint32_t use = j / NB;  // fill number of buffer b
+    CV* cur = bufs + (size_t)b * L * 8;
+    // a group may reach fill `use` of a buffer while fill `use - 1` (another
+    // group's tile) is still in flight, where the mbarrier parity would alias:
+    // first wait until that tile has been consumed and fill `use` issued
+    if (use > 0)
+      while (*(volatile uint32_t*)&issued[b] < use) {
+      }
+    mbar_wait(&full[b], use & 1);
+    const uint32_t tile = blockIdx.x + j * gridDim.x;
     const uint32_t o = tile / a.nchunk;
     const uint32_t z = (tile - o * a.nchunk) * 8 + col;
     CV v[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = cur[(t + m * T) * 8 + col];
-    __syncthreads();  // everyone holds its points: the buffer becomes the exchange buffer
-    tile_body<L, E, KIND, false, false>(a, v, t, o, z, true, tw, SmemStrided<CV, 8>{cur + col});
+    gsync();  // the group holds its points: the buffer becomes its exchange buffer
+    tile_body<L, E, KIND, false, false>(a, v, t, o, z, true, tw, SmemStrided<CV, 8>{cur + col}, gsync);
     const uint32_t obo = outer(a.lout, o) + z;
 #pragma unroll
     for (int m = 0; m < E; ++m) out[obo + inner<false>(a.lout, t + m * T)] = v[m];
-    __syncthreads();  // buffer free for the TMA issued at the next iteration
+    gsync();  // buffer released
+    if (lt == 0 && j + NB < nloc) {
+      issue(j + NB);
+      __threadfence_block();
+      *(volatile uint32_t*)&issued[b] = use + 1;
+    }
   }
 }
 
@@ -145,8 +182,10 @@ static cudaError_t launch_tma(const TileArgs& a, void* data, uint64_t d1, uint64
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  using Cfg = TmaCfg<L, CV>;
+  if constexpr (!Cfg::ok) return cudaErrorNotSupported;
   auto k = tma_tile_kernel<L, KIND, CV, AXIS>;
-  const size_t smem = 2 * (size_t)L * 8 * sizeof(CV) + 16;
+  const size_t smem = Cfg::smem;
   static cudaError_t init = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (init != cudaSuccess) return init;
   static int sms = [] {
@@ -157,7 +196,7 @@ static cudaError_t launch_tma(const TileArgs& a, void* data, uint64_t d1, uint64
   }();
   const uint32_t ntiles = a.n_outer * a.nchunk;
   const uint32_t grid = ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms;
-  k<<<grid, L, smem, st>>>(map, a, tw);
+  k<<<grid, L * Cfg::G, smem, st>>>(map, a, tw);
   return cudaGetLastError();
 }
 

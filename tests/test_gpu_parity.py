@@ -208,3 +208,25 @@ def test_complex64_fft_and_reductions():
     assert rel_l2(d.cpu().numpy(), np.fft.fftn(a.astype(np.complex128))) <= 1e-6
     w = qgrid.Wavefunction(a.copy(), grid)
     assert w.norm() == pytest.approx(float(np.sum(np.abs(a.astype(np.complex128)) ** 2) * grid.dvol), rel=1e-6)
+
+
+@pytest.mark.parametrize("precision", ["complex128", "complex64"])
+def test_regenerated_k2_matches_table_loads(monkeypatch, precision):
+    """The x pass regenerates kx^2, ky^2, kz^2 in registers once the plan has
+    verified numpy's (2 pi fftfreq)^2 tables bit for bit; forcing the table
+    loads (CTAP_KGEN=0) must give the identical wavefunction."""
+    n = (128, 64, 32)
+    grid = qgrid.make_grid(*n, (20e-6, 4e-6, 250e-6), origin=(-10e-6, 4e-6 / n[1] / 2, 0.0))
+    x, y, z = grid.x, grid.y, grid.z
+    v = 0.5 * M * ((2 * np.pi * 2e3) ** 2 * x[:, None, None] ** 2 + (2 * np.pi * 2e4) ** 2
+                   * (y[None, :, None] - 2e-6) ** 2 + (2 * np.pi * 20) ** 2 * (z[None, None, :] - 125e-6) ** 2)
+    psi0 = qgrid.gaussian_packet(grid, (-2e-6, 2e-6, 125e-6), (1e-6, 0.3e-6, 10e-6)).amplitudes
+
+    def run(kgen):
+        monkeypatch.setenv("CTAP_KGEN", kgen)
+        plan = propagator.make_plan(grid, v, M, 1e-6, precision=precision)
+        psi = qgrid.Wavefunction(psi0.copy(), grid)
+        psi, _ = propagator.evolve_real(psi, plan, 20)
+        return psi.amplitudes
+
+    assert np.array_equal(run("1"), run("0"))
