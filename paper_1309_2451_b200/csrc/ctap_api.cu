@@ -135,7 +135,15 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->twiddles, tw.size() * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(p->twiddles, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {  // complex64 copy of the (correctly rounded) double table
-    std::vector<float> tw32(tw.begin(), tw.end());
+    // float-float split of every (re, im): hi = rn(d), lo = rn(d - hi)
+    std::vector<float> tw32(2 * tw.size());
+    for (size_t i = 0; i < tw.size() / 2; ++i) {
+      const float hr = (float)tw[2 * i], hi = (float)tw[2 * i + 1];
+      tw32[4 * i + 0] = hr;
+      tw32[4 * i + 1] = hi;
+      tw32[4 * i + 2] = (float)(tw[2 * i] - (double)hr);
+      tw32[4 * i + 3] = (float)(tw[2 * i + 1] - (double)hi);
+    }
     e = cudaMalloc((void**)&p->twiddles32, tw32.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(p->twiddles32, tw32.data(), tw32.size() * sizeof(float), cudaMemcpyHostToDevice);
   }

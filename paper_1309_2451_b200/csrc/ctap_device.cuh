@@ -29,16 +29,25 @@ constexpr int kElems = 8;  // points per thread per line
 // scalar and builder.
 template <typename C>
 struct CT;
+// TW is the twiddle-table entry: double2, or for complex64 a float-float
+// pair (hi.x, hi.y, lo.x, lo.y) with hi + lo = the double twiddle to ~2^-48,
+// so no rounded twiddle (or constant) is applied to the data: a rounded
+// factor repeats every step at the same point and its ~3e-8 error would grow
+// linearly with the step count (the rounding of products only random-walks).
 template <>
 struct CT<double2> {
   using R = double;
+  using TW = double2;
   __device__ __forceinline__ static double2 mk(double a, double b) { return make_double2(a, b); }
 };
 template <>
 struct CT<float2> {
   using R = float;
+  using TW = float4;
   __device__ __forceinline__ static float2 mk(float a, float b) { return make_float2(a, b); }
 };
+template <typename C>
+using TwOf = typename CT<C>::TW;
 
 template <typename C>
 __device__ __forceinline__ C cadd(C a, C b) { return CT<C>::mk(a.x + b.x, a.y + b.y); }
@@ -60,6 +69,23 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, __fmul_rn(a.y, b.y)), fmaf(a.y, b.x, -__fmul_rn(a.x, b.y)));
 }
+// data x twiddle (DIR < 0) or x conj(twiddle) (DIR > 0)
+template <int DIR>
+__device__ __forceinline__ double2 tw_mul(double2 a, double2 w) { return DIR < 0 ? cmul(a, w) : cmulc(a, w); }
+template <int DIR>
+__device__ __forceinline__ float2 tw_mul(float2 a, float4 w) {
+  const float wy = DIR < 0 ? w.y : -w.y, ly = DIR < 0 ? w.w : -w.w;
+  // (a.x + i a.y)(hi + lo): the lo terms first, then the hi products on top
+  const float cx = fmaf(a.x, w.z, -__fmul_rn(a.y, ly));
+  const float cy = fmaf(a.x, ly, __fmul_rn(a.y, w.z));
+  return make_float2(fmaf(a.x, w.x, fmaf(-a.y, wy, cx)), fmaf(a.x, wy, fmaf(a.y, w.x, cy)));
+}
+// a * sqrt(1/2) (the radix-8 constant), with a single rounding in complex64
+__device__ __forceinline__ double mul_h(double a) { return 0.70710678118654752440 * a; }
+__device__ __forceinline__ float mul_h(float a) {
+  return fmaf(0x1.6a09e6p-1f, a, 0x1.9fcef4p-27f * a);  // hi + lo = sqrt(1/2) to 2^-48
+}
+
 // multiply by -i (DIR=-1, forward) or +i (DIR=+1, inverse)
 template <int DIR, typename C>
 __device__ __forceinline__ C mul_i(C a) {
@@ -100,8 +126,6 @@ template <int DIR>
 struct Dft<8, DIR> {
   template <typename C>
   __device__ __forceinline__ static void run(C* v) {
-    using R = typename CT<C>::R;
-    constexpr R h = (R)0.70710678118654752440;  // sqrt(2)/2
     C e[4] = {v[0], v[2], v[4], v[6]};
     C o[4] = {v[1], v[3], v[5], v[7]};
     Dft<4, DIR>::run(e);
@@ -109,11 +133,11 @@ struct Dft<8, DIR> {
     // o[k] *= exp(DIR i pi k / 4)
     C o1, o3;
     if (DIR < 0) {
-      o1 = CT<C>::mk(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-      o3 = CT<C>::mk(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+      o1 = CT<C>::mk(mul_h(o[1].x + o[1].y), mul_h(o[1].y - o[1].x));
+      o3 = CT<C>::mk(mul_h(o[3].y - o[3].x), -mul_h(o[3].x + o[3].y));
     } else {
-      o1 = CT<C>::mk(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y));
-      o3 = CT<C>::mk(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y));
+      o1 = CT<C>::mk(mul_h(o[1].x - o[1].y), mul_h(o[1].x + o[1].y));
+      o3 = CT<C>::mk(-mul_h(o[3].x + o[3].y), mul_h(o[3].x - o[3].y));
     }
     C o2 = mul_i<DIR>(o[2]);
     v[0] = cadd(e[0], o[0]);
@@ -192,7 +216,7 @@ struct SyncNamed {  // T threads (a multiple of 32) of one line: named barrier
 // Input: v[m] = x[t + m*T].  Output scattered to smem (unless last stage, in
 // which case v[m] = X[t + m*T] stays in registers).
 template <int L, int E, int R, int NS, int TWO, int DIR, bool LAST, typename C, typename Smem>
-__device__ __forceinline__ void stockham_stage(C* v, int t, const C* __restrict__ tw, Smem sm) {
+__device__ __forceinline__ void stockham_stage(C* v, int t, const TwOf<C>* __restrict__ tw, Smem sm) {
   constexpr int T = L / E;
   constexpr int NB = E / R;  // butterflies per thread
 #pragma unroll
@@ -206,8 +230,8 @@ __device__ __forceinline__ void stockham_stage(C* v, int t, const C* __restrict_
       // twiddle exp(DIR 2 pi i r k / (NS R)) from the stage-major table
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        C w = __ldg(&tw[TWO + (r - 1) * NS + k]);
-        u[r] = DIR < 0 ? cmul(u[r], w) : cmulc(u[r], w);
+        const TwOf<C> w = __ldg(&tw[TWO + (r - 1) * NS + k]);
+        u[r] = tw_mul<DIR>(u[r], w);
       }
     }
     Dft<R, DIR>::run(u);
@@ -223,7 +247,7 @@ __device__ __forceinline__ void stockham_stage(C* v, int t, const C* __restrict_
 }
 
 template <int L, int E, int S, int DIR, typename C, typename Smem, typename Sync>
-__device__ __forceinline__ void fft_stages(C* v, int t, const C* __restrict__ tw, Smem sm,
+__device__ __forceinline__ void fft_stages(C* v, int t, const TwOf<C>* __restrict__ tw, Smem sm,
                                            Sync sync) {
   using P = Plan<L, E>;
   constexpr int T = P::T;
@@ -248,7 +272,7 @@ __device__ __forceinline__ void fft_stages(C* v, int t, const C* __restrict__ tw
 // (barriers inside).  The radix plan (and hence the twiddle table) depends
 // only on L, not on E.
 template <int L, int DIR, int E = kElems, typename C, typename Smem, typename Sync>
-__device__ __forceinline__ void line_fft(C* v, int t, const C* __restrict__ tw, Smem sm, Sync sync) {
+__device__ __forceinline__ void line_fft(C* v, int t, const TwOf<C>* __restrict__ tw, Smem sm, Sync sync) {
   fft_stages<L, E, 0, DIR>(v, t, tw, sm, sync);
 }
 

@@ -56,7 +56,7 @@ struct ctap_plan {
   double kval[3];          // 1/(n d) per axis (numpy fftfreq's val)
   int dtype;               // CTAP_C128 or CTAP_C64
   double2* twiddles;       // stage-major twiddle tables for L = 8..1024
-  float2* twiddles32;      // the same, rounded to float (complex64 mode)
+  float4* twiddles32;      // the same as float-float pairs (complex64 mode)
   int tw_off[8];           // start of the table of L = 8 << i
   double2* kbuf;           // single-GPU k-space buffer (blocked layout, out of place y passes)
   int k_lx;                // log2 of the x block of the k-space layout (0: natural)

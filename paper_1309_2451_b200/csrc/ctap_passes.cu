@@ -76,7 +76,7 @@ struct ZArgs {
 
 template <int L, int KIND, bool VTAB, typename CV, typename Sync>
 __device__ __forceinline__ void z_body(const ZArgs& a, CV* v, int t, uint32_t off, bool active,
-                                       const CV* __restrict__ tw, SmemContig<CV> sm, Sync sync) {
+                                       const TwOf<CV>* __restrict__ tw, SmemContig<CV> sm, Sync sync) {
   constexpr int T = L / kElems;
   if constexpr (KIND == T_FWD) {
     line_fft<L, -1>(v, t, tw, sm, sync);
@@ -118,7 +118,7 @@ struct ZMinBlocks {
 };
 
 template <int L, int KIND, bool VTAB, typename CV>
-__global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::value) zline_kernel(ZArgs a, const CV* __restrict__ tw) {
+__global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::value) zline_kernel(ZArgs a, const TwOf<CV>* __restrict__ tw) {
   using Cfg = ZCfg<L, CV>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CV* smem = reinterpret_cast<CV*>(smem_raw);
@@ -169,7 +169,7 @@ struct TileCfg {
 template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W, bool PEERS = false>
 __global__ void __launch_bounds__(TileCfg<L, CV, W>::threads,
                                   KTAB ? TileCfg<L, CV, W>::minb_tab : TileCfg<L, CV, W>::minb)
-    tile_kernel(TileArgs a, const CV* __restrict__ tw) {
+    tile_kernel(TileArgs a, const TwOf<CV>* __restrict__ tw) {
   using Cfg = TileCfg<L, CV, W>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CV* smem = reinterpret_cast<CV*>(smem_raw);
@@ -219,7 +219,7 @@ static cudaError_t allow_smem(K k, size_t bytes) {
 }
 
 template <int L, int KIND, bool VTAB, typename CV>
-static cudaError_t launch_z(const ZArgs& a, const CV* tw, cudaStream_t st) {
+static cudaError_t launch_z(const ZArgs& a, const TwOf<CV>* tw, cudaStream_t st) {
   using Cfg = ZCfg<L, CV>;
   auto k = zline_kernel<L, KIND, VTAB, CV>;
   static cudaError_t init = allow_smem(k, Cfg::smem);
@@ -229,7 +229,7 @@ static cudaError_t launch_z(const ZArgs& a, const CV* tw, cudaStream_t st) {
 }
 
 template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W, bool PEERS = false>
-static cudaError_t launch_tile(const TileArgs& a, const CV* tw, cudaStream_t st) {
+static cudaError_t launch_tile(const TileArgs& a, const TwOf<CV>* tw, cudaStream_t st) {
   using Cfg = TileCfg<L, CV, W>;
   auto k = tile_kernel<L, KIND, PIN, POUT, KTAB, CV, W, PEERS>;
   static cudaError_t init = allow_smem(k, Cfg::smem);
@@ -255,7 +255,7 @@ static cudaError_t launch_tile(const TileArgs& a, const CV* tw, cudaStream_t st)
 // twiddle tables of both precisions for one line length
 struct Tw {
   const double2* d;
-  const float2* f;
+  const float4* f;
 };
 
 template <int KIND, bool VTAB>

@@ -70,7 +70,7 @@ struct TmaCfg {
 // AXIS 2: x pass on (x, y, z) (o = y, line = x = tensor dim 2)
 template <int L, int KIND, typename CV, int AXIS>
 __global__ void __launch_bounds__(L * TmaCfg<L, CV>::G, 1)
-    tma_tile_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a, const CV* __restrict__ tw) {
+    tma_tile_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a, const TwOf<CV>* __restrict__ tw) {
   using Cfg = TmaCfg<L, CV>;
   constexpr int E = kElems;
   constexpr int T = L / E;  // threads per column; a group is 8 T = L threads
@@ -164,7 +164,7 @@ static EncodeTiledFn encode_fn() {
 }
 
 template <int L, int KIND, typename CV, int AXIS>
-static cudaError_t launch_tma(const TileArgs& a, void* data, uint64_t d1, uint64_t d2, const CV* tw,
+static cudaError_t launch_tma(const TileArgs& a, void* data, uint64_t d1, uint64_t d2, const TwOf<CV>* tw,
                               cudaStream_t st) {
   constexpr int BOX = L < 256 ? L : 256;
   EncodeTiledFn enc = encode_fn();

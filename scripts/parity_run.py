@@ -7,6 +7,8 @@ cfg2b  128x128x256 Ioffe-floor harmonic (population-moving), 5000 steps / 25
 cfg2   128x128x256 scaled-chip CTAP (configs/scaled.cfg with n_y = 128),
        25,000 steps, PopulationRecorder every 50
 cfg3   256^3 paper-chip CTAP, 1000 steps / 100
+cfg4   512^3 paper-chip CTAP, 100 steps / 50 (V checked on 64^3 sampled points)
+cfg3c64 / cfg4c64  the same in complex64 mode, gate 1e-4 against the oracle
 
 Both sides start from the identical psi0 (host-built Gaussian) and V (device
 Biot-Savart kernel, checked bit-for-bit against the oracle's C restatement).
@@ -38,12 +40,13 @@ def chip(name):
     return dict(np.load(os.path.join(GOLDEN, f"segments_{name}.npz")))
 
 
-def run_case(name, grid, v, a0, steps, stride, half_gap, edge_threshold=None, v_check=None):
+def run_case(name, grid, v, a0, steps, stride, half_gap, edge_threshold=None, v_check=None,
+             precision="complex128"):
     og = orc.as_grid(grid)
     part = observables.symmetric_partition(grid, half_gap)
     # GPU
     psi = qgrid.Wavefunction(a0.copy(), grid)
-    plan = propagator.make_plan(grid, v, M, 1e-6)
+    plan = propagator.make_plan(grid, v, M, 1e-6, precision=precision)
     rec = observables.PopulationRecorder(part, stride=stride)
     obs = [rec]
     if edge_threshold is not None:
@@ -52,7 +55,9 @@ def run_case(name, grid, v, a0, steps, stride, half_gap, edge_threshold=None, v_
     t0 = time.perf_counter()
     psi, stats = propagator.evolve_real(psi, plan, steps, obs)
     t_gpu = time.perf_counter() - t0
-    got = psi.amplitudes.copy()
+    got = psi.amplitudes.astype(np.complex128)
+    del plan, psi
+    torch.cuda.empty_cache()
     rows_gpu = rec.trace.as_array()
     # CPU oracle
     v_host = v.cpu().numpy() if isinstance(v, torch.Tensor) else v
@@ -63,6 +68,7 @@ def run_case(name, grid, v, a0, steps, stride, half_gap, edge_threshold=None, v_
     ref, rows = orc.evolve_with_trace(a0.copy(), og, f, steps, stride, part.xb1, part.xb2)
     t_cpu = time.perf_counter() - t0
     rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+    gate_psi, gate_pop = (1e-10, 1e-9) if precision == "complex128" else (1e-4, 1e-4)
     dpop = float(np.abs(rows_gpu[:, 1:4] - rows[:, 1:4]).max())
     out = {
         "case": name, "grid": list(grid.n), "steps": steps, "stride": stride,
@@ -77,7 +83,8 @@ def run_case(name, grid, v, a0, steps, stride, half_gap, edge_threshold=None, v_
         "gpu_seconds": t_gpu, "gpu_steps_per_s": steps / t_gpu,
         "cpu_seconds": t_cpu, "cpu_steps_per_s": steps / t_cpu, "cpu_plan_seconds": t_plan,
         "cpu_threads": os.cpu_count(),
-        "pass": bool(rel <= 1e-10 and dpop <= 1e-9),
+        "precision": precision, "gates": [gate_psi, gate_pop],
+        "pass": bool(rel <= gate_psi and dpop <= gate_pop),
     }
     if v_check is not None:
         out["potential_check"] = v_check
@@ -135,6 +142,33 @@ def cfg3():
     v, check = chip_potential(grid, og, "paper", False)
     a0 = orc.gaussian_packet(og, (-7e-6, 1.43e-6, 200e-6), (0.25e-6, 0.12e-6, 15e-6))
     return run_case("cfg3 256^3 paper-chip CTAP", grid, v, a0, 1000, 100, 3.5e-6, v_check=check)
+
+
+def cfg3c64():
+    og = orc.Grid((256, 256, 256), (20e-6, 4e-6, 1000e-6), (-10e-6, 4e-6 / 512, 0.0))
+    grid = qgrid.SimGrid(og.n, og.extents, og.origin)
+    v, check = chip_potential(grid, og, "paper", False)
+    a0 = orc.gaussian_packet(og, (-7e-6, 1.43e-6, 200e-6), (0.25e-6, 0.12e-6, 15e-6))
+    return run_case("cfg3 256^3 paper-chip CTAP, complex64", grid, v, a0, 1000, 100, 3.5e-6, v_check=check,
+                    precision="complex64")
+
+
+def _cfg4(precision):
+    og = orc.Grid((512, 512, 512), (20e-6, 4e-6, 1000e-6), (-10e-6, 4e-6 / 1024, 0.0))
+    grid = qgrid.SimGrid(og.n, og.extents, og.origin)
+    v, check = chip_potential(grid, og, "paper", False)
+    a0 = orc.gaussian_packet(og, (-7e-6, 1.43e-6, 200e-6), (0.25e-6, 0.12e-6, 15e-6))
+    tag = "" if precision == "complex128" else ", complex64"
+    return run_case("cfg4 512^3 paper-chip CTAP" + tag, grid, v, a0, 100, 50, 3.5e-6, v_check=check,
+                    precision=precision)
+
+
+def cfg4():
+    return _cfg4("complex128")
+
+
+def cfg4c64():
+    return _cfg4("complex64")
 
 
 def main():
