@@ -190,6 +190,16 @@ CTAP_API int ctap_potential(const double* xs, int64_t nx, const double* ys, int6
                             double mu_eff, double mass, double omega_z, double z_center,
                             double pref, double* V_out, void* stream);
 
+/* Transverse minima of every z slice of V (the scan of _find_slice_minima,
+ * magfield.py:188-208, run by assemble_potential :239-240 for each slice).
+ * V_dev: (nx, ny, nz) float64.  count_dev[nz] (int64): number of interior
+ * points with V < V[i-1,j], V <= V[i+1,j], V < V[i,j-1], V <= V[i,j+1];
+ * best_dev[3 nz] (int64): row-major indices i*ny + j of the (up to) three
+ * lowest of them by (V, index), -1 padded.  The parabolic refinement and the
+ * x ordering of those points are host work (magfield.slice_minima). */
+CTAP_API int ctap_slice_minima(const double* V_dev, int64_t nx, int64_t ny, int64_t nz, int64_t* count_dev,
+                               int64_t* best_dev, void* stream);
+
 CTAP_API const char* ctap_last_error(void);
 CTAP_API const char* ctap_version(void);
 

@@ -20,6 +20,8 @@ cudaError_t ctap_run_potential(const double* xs, int64_t nx, const double* ys, i
                                int64_t nz, const double* seg_a, const double* seg_b, const double* seg_cur,
                                int64_t n_seg, double b0x, double b0y, double b0z, double mu_eff, double mass,
                                double omega_z, double z_center, double pref, double* V_out, cudaStream_t st);
+cudaError_t ctap_run_slice_minima(const double* V, int64_t nx, int64_t ny, int64_t nz, int64_t* count,
+                                  int64_t* best, cudaStream_t st);
 
 namespace {
 
@@ -390,6 +392,17 @@ CTAP_API int ctap_potential(const double* xs, int64_t nx, const double* ys, int6
   CUDA_TRY(ctap_run_potential(xs, nx, ys, ny, zs, nz, seg_a, seg_b, seg_cur, n_seg, b0x, b0y, b0z, mu_eff, mass,
                               omega_z, z_center, pref, V_out, (cudaStream_t)stream),
            "ctap_potential");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_slice_minima(const double* V_dev, int64_t nx, int64_t ny, int64_t nz, int64_t* count_dev,
+                               int64_t* best_dev, void* stream) {
+  if (!V_dev || !count_dev || !best_dev) return fail(CTAP_EINVAL, "null argument");
+  if (nx <= 0 || ny <= 0 || nz <= 0) return fail(CTAP_EINVAL, "empty grid");
+  if (nx * ny > (int64_t(1) << 31) || nz > (int64_t(1) << 30))
+    return fail(CTAP_EUNSUPPORTED, "slice too large");
+  CUDA_TRY(ctap_run_slice_minima(V_dev, nx, ny, nz, count_dev, best_dev, (cudaStream_t)stream),
+           "ctap_slice_minima");
   return CTAP_OK;
 }
 

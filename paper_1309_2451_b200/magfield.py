@@ -108,11 +108,81 @@ def potential_values(chip: ChipSegments, grid, x_slice=None) -> torch.Tensor:
     return potential_on_axes(chip, xs, ys, zs)
 
 
+class MinimumAbsentError(LookupError):
+    """The requested guide has no distinct transverse minimum (merged guides)."""
+
+
+@dataclass(frozen=True)
+class SliceMinima:
+    """Transverse minima of one z slice sorted by x, NaN padded to 3
+    (magfield.py:145-152)."""
+
+    x: np.ndarray       # (3,)
+    y: np.ndarray       # (3,)
+    value: np.ndarray   # (3,) J
+    n_guides: int
+
+
+def _refine(v_lo, v_mid, v_hi):
+    # parabolic vertex through three samples (magfield.py:180-186)
+    curv = v_lo - 2.0 * v_mid + v_hi
+    if curv <= 0:
+        return 0.0, 0.0
+    diff = v_lo - v_hi
+    return 0.5 * diff / curv, -0.125 * diff ** 2 / curv
+
+
+def slice_minima(values: torch.Tensor, grid) -> tuple:
+    """Per-z-slice transverse minima of V, as assemble_potential's
+    _find_slice_minima loop (magfield.py:188-208, :239-240).
+
+    The scan over every interior point of every slice (and the selection of
+    the three lowest minima) runs on the device (ctap_slice_minima); only
+    the <= 3 winners per slice and their 4-neighbours come back to the host
+    for the parabolic refinement, in the reference's float64 expressions.
+    Ties in V between a 3rd and 4th minimum are broken by row-major index
+    (numpy's argsort agrees for up to 16 minima per slice)."""
+    v = _device.to_device_f64(values)
+    nx, ny, nz = v.shape
+    count = torch.empty(nz, dtype=torch.int64, device=v.device)
+    best = torch.empty(3 * nz, dtype=torch.int64, device=v.device)
+    _lib.call("ctap_slice_minima", v.data_ptr(), nx, ny, nz, count.data_ptr(), best.data_ptr(),
+              _device.stream_handle())
+    best = best.view(nz, 3)
+    sel = best.clamp(min=0)
+    i, j = sel // ny, sel % ny
+    zz = torch.arange(nz, device=v.device)[:, None].expand(nz, 3)
+    # the 5-point stencil around each selected point (clamped for padding)
+    st = torch.stack([v[i, j, zz], v[(i - 1).clamp(min=0), j, zz], v[(i + 1).clamp(max=nx - 1), j, zz],
+                      v[i, (j - 1).clamp(min=0), zz], v[i, (j + 1).clamp(max=ny - 1), zz]])
+    st, count, best = (_device.to_host(t) for t in (st, count, best))
+    xs = np.asarray(grid.axis(0) if hasattr(grid, "axis") else grid.x)
+    ys = np.asarray(grid.axis(1) if hasattr(grid, "axis") else grid.y)
+    hx, hy = xs[1] - xs[0], ys[1] - ys[0]
+    out = []
+    for k in range(nz):
+        kept = [m for m in range(3) if best[k, m] >= 0]
+        if count[k] <= 3:  # all minima kept, in the reference's row-major order
+            kept.sort(key=lambda m: best[k, m])
+        res = np.full((3, 3), np.nan)
+        # x order; Python's sort is stable like numpy's argsort on <= 3 items
+        for slot, m in enumerate(sorted(kept, key=lambda m: xs[best[k, m] // ny])):
+            a, b = divmod(int(best[k, m]), ny)
+            vc, vxm, vxp, vym, vyp = (st[q, k, m] for q in range(5))
+            ox, dvx = _refine(vxm, vc, vxp)
+            oy, dvy = _refine(vym, vc, vyp)
+            res[0, slot] = xs[a] + ox * hx
+            res[1, slot] = ys[b] + oy * hy
+            res[2, slot] = vc + dvx + dvy
+        out.append(SliceMinima(res[0].copy(), res[1].copy(), res[2].copy(), len(kept)))
+    return tuple(out)
+
+
 @dataclass(frozen=True, eq=False)
 class PotentialGrid:
-    """Mirror of magfield.PotentialGrid (magfield.py:157-176): `values` is the
-    device tensor; `minima` is filled only when the reference's host minima
-    search is importable (out of the GPU scope)."""
+    """Mirror of magfield.PotentialGrid (magfield.py:155-176): `values` is the
+    device tensor; `minima` holds one SliceMinima per z slice (device scan,
+    slice_minima)."""
 
     values: torch.Tensor
     grid: object
@@ -122,17 +192,25 @@ class PotentialGrid:
     def host_values(self) -> np.ndarray:
         return _device.to_host(self.values)
 
+    def slice_minima(self, iz: int) -> SliceMinima:
+        return self.minima[iz]
 
-def assemble_potential(layout, grid, segments=None, with_minima: bool = False) -> PotentialGrid:
-    """assemble_potential (magfield.py:218-241) with V computed on the device.
+    def guide_minimum(self, iz: int, guide_index: int):
+        """(x, y, V) of guide 0/1/2 in slice iz (magfield.py:164-176)."""
+        m = self.minima[iz]
+        if guide_index >= max(m.n_guides, 0):
+            raise MinimumAbsentError(
+                f"slice {iz} has {m.n_guides} transverse minima (guides merged); "
+                f"guide {guide_index} absent")
+        return float(m.x[guide_index]), float(m.y[guide_index]), float(m.value[guide_index])
+
+
+def assemble_potential(layout, grid, segments=None, with_minima: bool = True) -> PotentialGrid:
+    """assemble_potential (magfield.py:218-241) with V and the per-slice
+    minima scan computed on the device.
 
     `layout` is a reference ChipLayout or a ChipSegments."""
     chip = layout if isinstance(layout, ChipSegments) else ChipSegments.from_layout(layout, segments)
     values = potential_values(chip, grid)
-    minima = None
-    if with_minima:
-        from ctapsim.magfield import _find_slice_minima  # reference host bookkeeping
-
-        v = _device.to_host(values)
-        minima = tuple(_find_slice_minima(v[:, :, iz], grid.x, grid.y) for iz in range(grid.n[2]))
+    minima = slice_minima(values, grid) if with_minima else None
     return PotentialGrid(values=values, grid=grid, layout=layout, minima=minima)

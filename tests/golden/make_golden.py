@@ -155,5 +155,68 @@ def main():
     save("gaussian_8x8x16.npz", **grid_arrays(g6), amps=gp.amplitudes)
 
 
+
+def minima_fixtures():
+    """Per-slice transverse minima (magfield._find_slice_minima through
+    assemble_potential) and build_partition, from the reference."""
+
+    def pack(pot, part=None, wires=None):
+        m = pot.minima
+        d = dict(V=pot.values, mx=np.array([s.x for s in m]), my=np.array([s.y for s in m]),
+                 mv=np.array([s.value for s in m]), mn=np.array([s.n_guides for s in m]))
+        if part is not None:
+            d.update(xb1=part.xb1, xb2=part.xb2, merged=part.merged, wire_pos=wires)
+        return d
+
+    out = {}
+    for cfg_name, n, tag in (("scaled.cfg", (64, 32, 64), "scaled"), ("paper.cfg", (64, 32, 64), "paper")):
+        cfg = config.load_config(os.path.join(CFG, cfg_name))
+        cfg = dataclasses.replace(cfg, n_x=n[0], n_y=n[1], n_z=n[2])
+        layout = cfg.to_layout()
+        grid = cfg.to_grid()
+        pot = magfield.assemble_potential(layout, grid)
+        part = observables.build_partition(pot)
+        wires = np.array([sorted(layout.wire_positions_at(float(z)).values()) for z in grid.z])
+        for k, v in pack(pot, part, wires).items():
+            out[f"{tag}_{k}"] = v
+        out[f"{tag}_n"] = np.array(grid.n)
+        out[f"{tag}_extents"] = np.array(grid.extents)
+        out[f"{tag}_origin"] = np.array(grid.origin)
+        print(tag, "slices with >=3 minima:", int((pot.minima and sum(s.n_guides >= 3 for s in pot.minima))),
+              "merged:", int(part.merged.sum()))
+    # synthetic slices: (a) small integer-valued slices full of exact ties
+    # (the < / <= pattern), redrawn until a slice has <= 3 minima so the
+    # reference's value argsort (whose tie order is numpy-build specific) is
+    # not involved, (b) continuous random slices with many minima
+    rng = np.random.default_rng(21)
+    ties = np.empty((8, 8, 64))
+    for k in range(ties.shape[2]):
+        while True:
+            s = rng.integers(0, 3, size=(8, 8)).astype(float)
+            c = s[1:-1, 1:-1]
+            cnt = int(((c < s[:-2, 1:-1]) & (c <= s[2:, 1:-1]) & (c < s[1:-1, :-2]) & (c <= s[1:-1, 2:])).sum())
+            if cnt <= 3:
+                break
+        ties[:, :, k] = s
+    smooth = rng.standard_normal((64, 32, 16))
+    for tag, v in (("ties", ties), ("many", smooth)):
+        g = qgrid.make_grid(v.shape[0], v.shape[1], v.shape[2],
+                            (20e-6, 4e-6, 100e-6), origin=(-10e-6, 0.1e-6, 0.0))
+        pot = magfield.PotentialGrid(values=v, grid=g, layout=None,
+                                     minima=tuple(magfield._find_slice_minima(v[:, :, k], g.x, g.y)
+                                                  for k in range(v.shape[2])))
+        for k, a in pack(pot).items():
+            out[f"{tag}_{k}"] = a
+        out[f"{tag}_n"] = np.array(g.n)
+        out[f"{tag}_extents"] = np.array(g.extents)
+        out[f"{tag}_origin"] = np.array(g.origin)
+        print(tag, "max minima per slice:", int(out[f"{tag}_mn"].max()))
+    save("minima.npz", **out)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["minima"]:
+        minima_fixtures()
+    else:
+        main()
+        minima_fixtures()
