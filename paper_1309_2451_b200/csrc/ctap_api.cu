@@ -133,6 +133,9 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   p->kgen = 1;
   for (int i = 0; i < 3; ++i) p->kgen &= recover_kval(k2h[i], d->n[i], &p->kval[i]);
   if (const char* env = getenv("CTAP_KGEN")) p->kgen &= atoi(env) != 0;
+  p->zchunk = 0;
+  if (const char* env = getenv("CTAP_ZCHUNK")) p->zchunk = atoll(env);
+  if (p->zchunk % 8 || p->zchunk < 0 || (p->zchunk && d->n[2] % p->zchunk)) p->zchunk = 0;
   std::vector<double> tw = ctap_make_twiddles(p->tw_off);
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->twiddles, tw.size() * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(p->twiddles, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice);
@@ -201,6 +204,10 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
   cudaFree(p->kbuf);
   if (p->g_exec) cudaGraphExecDestroy(p->g_exec);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  for (int i = 0; i < 2; ++i)
+    if (p->kin_stream[i]) cudaStreamDestroy(p->kin_stream[i]);
+  for (int i = 0; i < 3; ++i)
+    if (p->kin_ev[i]) cudaEventDestroy(p->kin_ev[i]);
   delete p;
   return CTAP_OK;
 }
@@ -225,6 +232,41 @@ CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, vo
   return CTAP_OK;
 }
 
+// y, [x K x^-1], y^-1 of one step.  With p->zchunk = W the three passes run
+// per z chunk of W columns, so a chunk (nx ny W points) stays in L2 from the
+// y pass to the y^-1 pass instead of making three HBM round trips.
+static cudaError_t kin_block(ctap_plan* p, void* psi, cudaStream_t st) {
+  const int64_t nz = p->n[2], W = p->zchunk;
+  if (W <= 0 || W >= nz) {
+    cudaError_t e = ctap_run_pass(p, CTAP_PASS_Y_FWD, psi, psi, st);
+    if (e == cudaSuccess) e = ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, st);
+    if (e == cudaSuccess) e = ctap_run_pass(p, CTAP_PASS_Y_INV, psi, psi, st);
+    return e;
+  }
+  // chunks alternate between two streams forked from (and joined back into)
+  // st, so the FP64-bound x pass of one chunk co-runs with the HBM-bound y
+  // passes of its neighbours (inside a graph capture this becomes two
+  // parallel branches)
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+    if (!p->kin_stream[i]) e = cudaStreamCreateWithFlags(&p->kin_stream[i], cudaStreamNonBlocking);
+  for (int i = 0; i < 3 && e == cudaSuccess; ++i)
+    if (!p->kin_ev[i]) e = cudaEventCreateWithFlags(&p->kin_ev[i], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(p->kin_ev[0], st);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(p->kin_stream[i], p->kin_ev[0], 0);
+  for (int64_t z0 = 0, c = 0; z0 < nz && e == cudaSuccess; z0 += W, ++c) {
+    cudaStream_t s = p->kin_stream[c & 1];
+    e = ctap_run_pass_z(p, CTAP_PASS_Y_FWD, psi, psi, z0, W, s);
+    if (e == cudaSuccess) e = ctap_run_pass_z(p, CTAP_PASS_X_KIN, psi, psi, z0, W, s);
+    if (e == cudaSuccess) e = ctap_run_pass_z(p, CTAP_PASS_Y_INV, psi, psi, z0, W, s);
+  }
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventRecord(p->kin_ev[1 + i], p->kin_stream[i]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, p->kin_ev[1 + i], 0);
+  }
+  return e;
+}
+
 CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
   if (!p || !psi) return fail(CTAP_EINVAL, "null argument");
   if (n < 0) return fail(CTAP_EINVAL, "n_steps must be >= 0");
@@ -245,9 +287,7 @@ CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
       CUDA_TRY(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal), "ctap_advance capture");
       cudaError_t ce = cudaSuccess;
       for (int m = 0; m < kGraphSteps && ce == cudaSuccess; ++m) {
-        ce = ctap_run_pass(p, CTAP_PASS_Y_FWD, psi, psi, p->cap_stream);
-        if (ce == cudaSuccess) ce = ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, p->cap_stream);
-        if (ce == cudaSuccess) ce = ctap_run_pass(p, CTAP_PASS_Y_INV, psi, psi, p->cap_stream);
+        ce = kin_block(p, psi, p->cap_stream);
         if (ce == cudaSuccess) ce = ctap_run_pass(p, CTAP_PASS_Z_MID, psi, psi, p->cap_stream);
       }
       cudaError_t ee = cudaStreamEndCapture(p->cap_stream, &g);
@@ -269,9 +309,7 @@ CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
       CUDA_TRY(ctap_run_pass(p, ctap::PASS_X_KIN_BLK, p->kbuf, p->kbuf, st), "ctap_advance");
       CUDA_TRY(ctap_run_pass(p, ctap::PASS_Y_INV_BLK, p->kbuf, psi, st), "ctap_advance");
     } else {
-      CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Y_FWD, psi, psi, st), "ctap_advance");
-      CUDA_TRY(ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, st), "ctap_advance");
-      CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Y_INV, psi, psi, st), "ctap_advance");
+      CUDA_TRY(kin_block(p, psi, st), "ctap_advance");
     }
     CUDA_TRY(ctap_run_pass(p, j < n - 1 ? CTAP_PASS_Z_MID : CTAP_PASS_Z_LAST, psi, psi, st), "ctap_advance");
   }

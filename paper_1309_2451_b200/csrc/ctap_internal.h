@@ -53,6 +53,7 @@ struct ctap_plan {
   void* expk_dev;          // optional table exp(-i k^2 dt/2) / N, x-pass layout
   double* k2_dev[3];       // squared wavenumbers per axis (global lengths)
   int kgen;                // k^2 regenerated on device from kval (tables verified)
+  int64_t zchunk;          // kinetic block in z chunks of this width (0: whole volume)
   double kval[3];          // 1/(n d) per axis (numpy fftfreq's val)
   int dtype;               // CTAP_C128 or CTAP_C64
   double2* twiddles;       // stage-major twiddle tables for L = 8..1024
@@ -66,6 +67,8 @@ struct ctap_plan {
   // CUDA graph of M interior steps (launch-bound small grids), captured on a
   // private stream for one psi pointer and replayed on the caller's stream
   cudaStream_t cap_stream;
+  cudaStream_t kin_stream[2];  // z-chunked kinetic block: two concurrent chunk pipelines
+  cudaEvent_t kin_ev[3];
   cudaGraphExec_t g_exec;
   const void* g_psi;
   int g_steps;
@@ -78,3 +81,5 @@ cudaError_t ctap_run_phase_table(const ctap_plan* p, int which, void* out, cudaS
 #include <vector>
 std::vector<double> ctap_make_twiddles(int off[8]);
 cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* out, cudaStream_t st);
+cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* out, int64_t z0, int64_t zn,
+                            cudaStream_t st);

@@ -396,13 +396,25 @@ static Tw twid(const ctap_plan* p, int64_t L) {
   return Tw{p->twiddles + off, p->twiddles32 + off};
 }
 
+cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* out, int64_t z0, int64_t zn,
+                            cudaStream_t st);
+
 cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* out, cudaStream_t st) {
+  return ctap_run_pass_z(p, kind, in, out, 0, p->n[2], st);
+}
+
+// A strided pass restricted to the z columns [z0, z0 + zn) (zn a multiple of
+// 8): the kinetic block of the step can then run chunk by chunk with the
+// chunk's data resident in L2 between its y, x and y^-1 passes.
+cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* out, int64_t z0, int64_t zn,
+                            cudaStream_t st) {
   const int64_t nx = p->n[0], ny = p->n[1], nz = p->n[2];
+  const bool zsub = z0 != 0 || zn != nz;
   const bool c64 = p->dtype == CTAP_C64;
   const size_t csz = c64 ? sizeof(float2) : sizeof(double2);
   const Tw tw_any = twid(p, 8);
   // x passes read 16-column (instead of 8) tiles when z allows it
-  const bool xw16 = CTAP_XW == 16 && nz >= 16;
+  const bool xw16 = CTAP_XW == 16 && nz >= 16 && !zsub;
   // strided passes on natural layouts go through the TMA pipeline in
   // complex64 (CTAP_TMA=1, default); in complex128 the register-fed
   // tile_kernel measured faster (CTAP_TMA=2 adds c128 x, 3 c128 x and y;
@@ -411,9 +423,9 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
     const char* e = getenv("CTAP_TMA");
     return e ? atoi(e) : CTAP_TMA_DEFAULT;
   }();
-  const bool use_tma = tma_mode != 0;
+  const bool use_tma = tma_mode != 0 && !zsub;
 
-  const bool use_tma_x = tma_mode >= 2 || (tma_mode == 1 && c64);
+  const bool use_tma_x = !zsub && (tma_mode >= 2 || (tma_mode == 1 && c64));
   const int P = p->slab_p;
   const uint32_t nxl = (uint32_t)(nx / P), nyl = (uint32_t)(ny / P);
   PhaseArgs ph;
@@ -429,6 +441,7 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
   ph.imag = p->mode == 1;
   ph.outer_off = 0;
   ph.kgen = p->kgen;
+  ph.z_off = (uint32_t)z0;
   for (int i = 0; i < 3; ++i) {
     ph.kn[i] = (uint32_t)p->n[i];
     ph.kval[i] = p->kval[i];
@@ -452,10 +465,12 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
     }
     return cudaErrorInvalidValue;
   }
+  if (zsub && (kind < PASS_Y_FWD || kind > PASS_X_INV || (zn & 7) || z0 < 0 || z0 + zn > nz))
+    return cudaErrorInvalidValue;
   TileArgs a;
-  a.in = in;
-  a.out = out;
-  a.nchunk = (uint32_t)(nz / 8);
+  a.in = (const char*)in + csz * (size_t)z0;
+  a.out = (char*)out + csz * (size_t)z0;
+  a.nchunk = (uint32_t)(zn / 8);
   a.ph = ph;
   const uint32_t NZ = (uint32_t)nz, NY = (uint32_t)ny;
   constexpr int kNone = 31;  // no outer blocking

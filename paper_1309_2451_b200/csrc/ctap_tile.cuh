@@ -24,6 +24,7 @@ struct PhaseArgs {
   // k^2 regenerated in registers instead of loaded (kgen != 0): the plan
   // verified that (2 pi * (m * kval[a]))^2 reproduces every table entry
   int kgen;
+  uint32_t z_off;  // global z of the pass's column 0 (z-chunked passes)
   uint32_t kn[3];
   double kval[3];
 };
@@ -137,10 +138,10 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, CV* v, int t, uint3
         f[m] = active ? __ldcg(&expk[outer(a.lout, o) + inner<KBLK>(a.lout, t + m * T) + z]) : CT<CV>::mk(0, 0);
     } else if (a.ph.kgen) {
       ky2 = k2_gen(a.ph.outer_off + o, a.ph.kn[1], a.ph.kval[1]);
-      kz2 = k2_gen(z, a.ph.kn[2], a.ph.kval[2]);
+      kz2 = k2_gen(a.ph.z_off + z, a.ph.kn[2], a.ph.kval[2]);
     } else {
       ky2 = __ldg(&a.ph.ky2[a.ph.outer_off + o]);
-      kz2 = __ldg(&a.ph.kz2[z]);
+      kz2 = __ldg(&a.ph.kz2[a.ph.z_off + z]);
     }
     line_fft<L, -1, E>(v, t, tw, sm, sync);
     if (active) {

@@ -230,3 +230,25 @@ def test_regenerated_k2_matches_table_loads(monkeypatch, precision):
         return psi.amplitudes
 
     assert np.array_equal(run("1"), run("0"))
+
+
+@pytest.mark.parametrize("precision", ["complex128", "complex64"])
+def test_zchunked_kinetic_block_bitwise(monkeypatch, precision):
+    """CTAP_ZCHUNK runs y, [x K x^-1], y^-1 per z chunk on two forked streams
+    (an experiment kept behind a switch); the result must not change."""
+    n = (64, 32, 64)
+    grid = qgrid.make_grid(*n, (20e-6, 4e-6, 250e-6), origin=(-10e-6, 4e-6 / n[1] / 2, 0.0))
+    rng = np.random.default_rng(3)
+    v = 1e-30 * (1.0 + rng.random(n))
+    a0 = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+
+    def run(w):
+        monkeypatch.setenv("CTAP_ZCHUNK", w)
+        plan = propagator.make_plan(grid, v, M, 1e-6, precision=precision)
+        psi = qgrid.Wavefunction(a0.copy(), grid)
+        psi, _ = propagator.evolve_real(psi, plan, 40)
+        return psi.amplitudes
+
+    ref = run("0")
+    assert np.array_equal(run("16"), ref)
+    assert np.array_equal(run("32"), ref)
