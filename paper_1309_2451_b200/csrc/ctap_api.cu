@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "ctap_internal.h"
+#include "ctap_sincos_tab.h"
 
 cudaError_t ctap_run_observe(const ctap_plan* p, const void* psi, const double* xs, const double* xb1,
                              const double* xb2, int margin, double* out, cudaStream_t st);
@@ -136,6 +137,17 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   p->zchunk = 0;
   if (const char* env = getenv("CTAP_ZCHUNK")) p->zchunk = atoll(env);
   if (p->zchunk % 8 || p->zchunk < 0 || (p->zchunk && d->n[2] % p->zchunk)) p->zchunk = 0;
+  {  // sincos rotation tables: unscaled (V phases) and times 1/N (K phase)
+    std::vector<double> sc(4 * 256);
+    for (int k = 0; k < 256; ++k) {
+      sc[2 * k] = kSinCos256[k][0];
+      sc[2 * k + 1] = kSinCos256[k][1];
+      sc[512 + 2 * k] = kSinCos256[k][0] * p->inv_scale;  // exact: power of two
+      sc[512 + 2 * k + 1] = kSinCos256[k][1] * p->inv_scale;
+    }
+    if (e == cudaSuccess) e = cudaMalloc((void**)&p->sctab, sc.size() * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(p->sctab, sc.data(), sc.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
   std::vector<double> tw = ctap_make_twiddles(p->tw_off);
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->twiddles, tw.size() * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(p->twiddles, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice);
@@ -197,6 +209,7 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
   for (int i = 0; i < 3; ++i) cudaFree(p->k2_dev[i]);
   cudaFree(p->twiddles);
   cudaFree(p->twiddles32);
+  cudaFree(p->sctab);
   cudaFree(p->red_partial);
   cudaFree(p->vi_dev);
   cudaFree(p->expv_dev);

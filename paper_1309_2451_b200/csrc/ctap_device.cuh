@@ -80,12 +80,16 @@ __device__ __forceinline__ float2 tw_mul(float2 a, float4 w) {
   const float cy = fmaf(a.x, ly, __fmul_rn(a.y, w.z));
   return make_float2(fmaf(a.x, w.x, fmaf(-a.y, wy, cx)), fmaf(a.x, wy, fmaf(a.y, w.x, cy)));
 }
-// a * sqrt(1/2) (the radix-8 constant), with a single rounding in complex64
-__device__ __forceinline__ double mul_h(double a) { return 0.70710678118654752440 * a; }
-__device__ __forceinline__ float mul_h(float a) {
-  return fmaf(0x1.6a09e6p-1f, a, 0x1.9fcef4p-27f * a);  // hi + lo = sqrt(1/2) to 2^-48
+// sqrt(1/2) * a + b (the radix-8 constant).  complex128: one fused rounding.
+// complex64: hi + lo = sqrt(1/2) to 2^-48 so no rounded constant is applied
+// to the data; the product is rounded first (inside the fma the exact hi*a
+// keeps the bits that carry lo*a through the rounding), then b is added --
+// folding b into the inner fma instead would round lo*a away against b
+// every time, i.e. apply hi alone (a systematic 1.2e-8 per use).
+__device__ __forceinline__ double fma_h(double a, double b) { return fma(0.70710678118654752440, a, b); }
+__device__ __forceinline__ float fma_h(float a, float b) {
+  return fmaf(0x1.6a09e6p-1f, a, 0x1.9fcef4p-27f * a) + b;
 }
-
 // multiply by -i (DIR=-1, forward) or +i (DIR=+1, inverse)
 template <int DIR, typename C>
 __device__ __forceinline__ C mul_i(C a) {
@@ -130,24 +134,30 @@ struct Dft<8, DIR> {
     C o[4] = {v[1], v[3], v[5], v[7]};
     Dft<4, DIR>::run(e);
     Dft<4, DIR>::run(o);
-    // o[k] *= exp(DIR i pi k / 4)
-    C o1, o3;
+    // o[k] *= exp(DIR i pi k / 4); the sqrt(1/2) of k = 1, 3 is fused into
+    // the final additions (h s + e with one rounding)
+    using R = typename CT<C>::R;
+    R s1, d1, s3, d3;  // o1 = h (s1, d1), o3 = h (s3, d3)
     if (DIR < 0) {
-      o1 = CT<C>::mk(mul_h(o[1].x + o[1].y), mul_h(o[1].y - o[1].x));
-      o3 = CT<C>::mk(mul_h(o[3].y - o[3].x), -mul_h(o[3].x + o[3].y));
+      s1 = o[1].x + o[1].y;
+      d1 = o[1].y - o[1].x;
+      s3 = o[3].y - o[3].x;
+      d3 = -(o[3].x + o[3].y);
     } else {
-      o1 = CT<C>::mk(mul_h(o[1].x - o[1].y), mul_h(o[1].x + o[1].y));
-      o3 = CT<C>::mk(-mul_h(o[3].x + o[3].y), mul_h(o[3].x - o[3].y));
+      s1 = o[1].x - o[1].y;
+      d1 = o[1].x + o[1].y;
+      s3 = -(o[3].x + o[3].y);
+      d3 = o[3].x - o[3].y;
     }
     C o2 = mul_i<DIR>(o[2]);
     v[0] = cadd(e[0], o[0]);
     v[4] = csub(e[0], o[0]);
-    v[1] = cadd(e[1], o1);
-    v[5] = csub(e[1], o1);
+    v[1] = CT<C>::mk(fma_h(s1, e[1].x), fma_h(d1, e[1].y));
+    v[5] = CT<C>::mk(fma_h(-s1, e[1].x), fma_h(-d1, e[1].y));
     v[2] = cadd(e[2], o2);
     v[6] = csub(e[2], o2);
-    v[3] = cadd(e[3], o3);
-    v[7] = csub(e[3], o3);
+    v[3] = CT<C>::mk(fma_h(s3, e[3].x), fma_h(d3, e[3].y));
+    v[7] = CT<C>::mk(fma_h(-s3, e[3].x), fma_h(-d3, e[3].y));
   }
 };
 
@@ -297,123 +307,58 @@ __device__ __forceinline__ double k_phase(double kx2, double ky2, double kz2, do
   return __dmul_rn(__dmul_rn(-0.5, __dmul_rn(k2, len2)), dt_i);
 }
 
-// cos/sin(k pi/32), k = 0..63, correctly rounded (50-digit decimal series)
-__device__ const double2 kSinCosTab[64] = {
-    {1.0, 0.0},
-    {0.9951847266721969, 0.0980171403295606},
-    {0.9807852804032304, 0.19509032201612828},
-    {0.9569403357322088, 0.2902846772544624},
-    {0.9238795325112867, 0.3826834323650898},
-    {0.881921264348355, 0.47139673682599764},
-    {0.8314696123025452, 0.5555702330196022},
-    {0.773010453362737, 0.6343932841636455},
-    {0.7071067811865476, 0.7071067811865476},
-    {0.6343932841636455, 0.773010453362737},
-    {0.5555702330196022, 0.8314696123025452},
-    {0.47139673682599764, 0.881921264348355},
-    {0.3826834323650898, 0.9238795325112867},
-    {0.2902846772544624, 0.9569403357322088},
-    {0.19509032201612828, 0.9807852804032304},
-    {0.0980171403295606, 0.9951847266721969},
-    {2.1014944983910808e-55, 1.0},
-    {-0.0980171403295606, 0.9951847266721969},
-    {-0.19509032201612828, 0.9807852804032304},
-    {-0.2902846772544624, 0.9569403357322088},
-    {-0.3826834323650898, 0.9238795325112867},
-    {-0.47139673682599764, 0.881921264348355},
-    {-0.5555702330196022, 0.8314696123025452},
-    {-0.6343932841636455, 0.773010453362737},
-    {-0.7071067811865476, 0.7071067811865476},
-    {-0.773010453362737, 0.6343932841636455},
-    {-0.8314696123025452, 0.5555702330196022},
-    {-0.881921264348355, 0.47139673682599764},
-    {-0.9238795325112867, 0.3826834323650898},
-    {-0.9569403357322088, 0.2902846772544624},
-    {-0.9807852804032304, 0.19509032201612828},
-    {-0.9951847266721969, 0.0980171403295606},
-    {-1.0, -4.164292633035009e-54},
-    {-0.9951847266721969, -0.0980171403295606},
-    {-0.9807852804032304, -0.19509032201612828},
-    {-0.9569403357322088, -0.2902846772544624},
-    {-0.9238795325112867, -0.3826834323650898},
-    {-0.881921264348355, -0.47139673682599764},
-    {-0.8314696123025452, -0.5555702330196022},
-    {-0.773010453362737, -0.6343932841636455},
-    {-0.7071067811865476, -0.7071067811865476},
-    {-0.6343932841636455, -0.773010453362737},
-    {-0.5555702330196022, -0.8314696123025452},
-    {-0.47139673682599764, -0.881921264348355},
-    {-0.3826834323650898, -0.9238795325112867},
-    {-0.2902846772544624, -0.9569403357322088},
-    {-0.19509032201612828, -0.9807852804032304},
-    {-0.0980171403295606, -0.9951847266721969},
-    {1.1132433694450584e-53, -1.0},
-    {0.0980171403295606, -0.9951847266721969},
-    {0.19509032201612828, -0.9807852804032304},
-    {0.2902846772544624, -0.9569403357322088},
-    {0.3826834323650898, -0.9238795325112867},
-    {0.47139673682599764, -0.881921264348355},
-    {0.5555702330196022, -0.8314696123025452},
-    {0.6343932841636455, -0.773010453362737},
-    {0.7071067811865476, -0.7071067811865476},
-    {0.773010453362737, -0.6343932841636455},
-    {0.8314696123025452, -0.5555702330196022},
-    {0.881921264348355, -0.47139673682599764},
-    {0.9238795325112867, -0.3826834323650898},
-    {0.9569403357322088, -0.2902846772544624},
-    {0.9807852804032304, -0.19509032201612828},
-    {0.9951847266721969, -0.0980171403295606}
-};
 
 // polynomial/reduction constants as constant-bank operands (no per-use
 // register materialisation)
-__constant__ double kSC[12] = {
-    10.185916357881302,        // 0: 32/pi
-    0x1.921fb54000000p-4,      // 1: pi/32 = C1 + C2 + C3 (27 + 27 + 53 bits)
-    0x1.10b4610000000p-34,     // 2
-    0x1.a62633145c06ep-62,     // 3
-    2.7557319223985893e-06,    // 4: 1/9!
-    -1.9841269841269841e-04,   // 5: -1/7!
-    8.3333333333333333e-03,    // 6: 1/5!
-    -1.6666666666666666e-01,   // 7: -1/3!
-    2.4801587301587302e-05,    // 8: 1/8!
-    -1.3888888888888889e-03,   // 9: -1/6!
-    4.1666666666666664e-02,    // 10: 1/4!
-    6755399441055744.0,        // 11: 1.5 * 2^52
+__constant__ double kSC[10] = {
+    40.74366543152521,         // 0: 128/pi
+    0x1.921fb54000000p-6,      // 1: pi/128 = C1 + C2 + C3 (27 + 27 + 53 bits)
+    0x1.10b4610000000p-36,     // 2
+    0x1.a62633145c06ep-64,     // 3
+    -1.9841269841269841e-04,   // 4: -1/7!
+    8.3333333333333333e-03,    // 5: 1/5!
+    -1.6666666666666666e-01,   // 6: -1/3!
+    -1.3888888888888889e-03,   // 7: -1/6!
+    4.1666666666666664e-02,    // 8: 1/4!
+    6755399441055744.0,        // 9: 1.5 * 2^52
 };
 
 // sincos for the phase factors.  The phase itself is exact (computed with the
 // recipes above); only cos/sin of it are evaluated here, to ~1.5 ulp:
-//   n = rint(phi * 32/pi) via the 1.5*2^52 magic constant, r = phi - n*pi/32
+//   n = rint(phi * 128/pi) via the 1.5*2^52 magic constant, r = phi - n*pi/128
 //   by a three-term Cody-Waite split (exact first term for |n| < 2^26),
-//   Taylor polynomials on |r| <= pi/64 (sin to r^9, cos to r^8), and a
-//   rotation by the tabulated (cos, sin)(n pi/32).
-// About 19 FP64 operations against ~40 FP64 + ~70 other instructions for the
-// library sincos; |phi| >= 2^22 falls back to the library (never on CTAP
-// grids, where |phi| < 1e6).  Errors of an ulp in the factor are harmless
-// (only the phase must be bit-exact).
-__device__ __forceinline__ void fast_sincos(double phi, double* s, double* c) {
-  if (fabs(phi) < 4194304.0) {
-    const double t = fma(phi, kSC[0], kSC[11]);
+//   Taylor polynomials on |r| <= pi/256 (sin to r^7, cos to r^6; the next
+//   terms are below 1e-20), and a rotation by tab[n & 255] = f (cos, sin)(n pi/128)
+//   where f is a per-plan factor (1, or the kinetic step's 1/N folded in -- a
+//   power of two, so the folding is exact).
+// 16 FP64 operations against ~40 FP64 + ~70 other instructions for the library
+// sincos; |phi| >= 2^20 falls back to the library (never on CTAP grids, where
+// |phi| < 1e6) and applies f = tab[0].x explicitly.  Errors of an ulp in the
+// factor are harmless (only the phase must be bit-exact).
+__device__ __forceinline__ void fast_sincos(double phi, const double2* __restrict__ tab, double* s, double* c) {
+  if (fabs(phi) < 1048576.0) {
+    const double t = fma(phi, kSC[0], kSC[9]);
     const int n = __double2loint(t);
-    const double nf = t - kSC[11];
+    const double nf = t - kSC[9];
     double r = fma(-nf, kSC[1], phi);
     r = fma(-nf, kSC[2], r);
     r = fma(-nf, kSC[3], r);
     const double r2 = r * r;
     double ps = fma(r2, kSC[4], kSC[5]);
     ps = fma(r2, ps, kSC[6]);
-    ps = fma(r2, ps, kSC[7]);
     const double sr = fma(r * r2, ps, r);
-    double pc = fma(r2, kSC[8], kSC[9]);
-    pc = fma(r2, pc, kSC[10]);
+    double pc = fma(r2, kSC[7], kSC[8]);
     pc = fma(r2, pc, -0.5);
     const double cr = fma(r2, pc, 1.0);
-    const double2 tb = __ldg(&kSinCosTab[n & 63]);
+    const double2 tb = __ldg(&tab[n & 255]);
     *c = fma(tb.x, cr, -(tb.y * sr));
     *s = fma(tb.y, cr, tb.x * sr);
   } else {
-    sincos(phi, s, c);
+    double ss, cc;
+    sincos(phi, &ss, &cc);
+    const double f = __ldg(&tab[0].x);
+    *s = ss * f;
+    *c = cc * f;
   }
 }
 

@@ -52,6 +52,7 @@ struct ctap_plan {
   void* expv_dev;          // optional table exp(-i v_i dt_i), plan precision (phase_tables, real time)
   void* expk_dev;          // optional table exp(-i k^2 dt/2) / N, x-pass layout
   double* k2_dev[3];       // squared wavenumbers per axis (global lengths)
+  double2* sctab;          // [256] (cos, sin)(k pi/128), [256] the same times 1/N
   int kgen;                // k^2 regenerated on device from kval (tables verified)
   int64_t zchunk;          // kinetic block in z chunks of this width (0: whole volume)
   double kval[3];          // 1/(n d) per axis (numpy fftfreq's val)

@@ -287,7 +287,7 @@ __global__ void phase_field_kernel(CV* __restrict__ out, const double* __restric
                                    const double* __restrict__ kx2, const double* __restrict__ ky2,
                                    const double* __restrict__ kz2, uint32_t nx, uint32_t ny, uint32_t nz,
                                    uint32_t x_off, uint32_t y_off, int which, int imag, double dt_i,
-                                   double len2, double scale, int lx) {
+                                   double len2, double scale, int lx, const double2* __restrict__ sct) {
   using R = typename CT<CV>::R;
   const uint32_t n = nx * ny * nz;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -305,7 +305,7 @@ __global__ void phase_field_kernel(CV* __restrict__ out, const double* __restric
       out[dst] = CT<CV>::mk((R)(exp(phi) * scale), (R)0);
     } else {
       double s, c;
-      fast_sincos(phi, &s, &c);
+      fast_sincos(phi, sct, &s, &c);
       out[dst] = CT<CV>::mk((R)(c * scale), (R)(s * scale));
     }
   }
@@ -368,12 +368,13 @@ static cudaError_t phase_field(const ctap_plan* p, int which, void* out, cudaStr
     const uint32_t nyl = (uint32_t)(p->n[1] / p->slab_p);
     phase_field_kernel<CV><<<p->red_blocks, 256, 0, st>>>(
         (CV*)out, p->vi_dev, p->k2_dev[0], p->k2_dev[1], p->k2_dev[2], (uint32_t)p->n[0], nyl,
-        (uint32_t)p->n[2], 0u, (uint32_t)p->slab_r * nyl, 2, imag, p->dt_i, p->len2, p->inv_scale, p->k_lx);
+        (uint32_t)p->n[2], 0u, (uint32_t)p->slab_r * nyl, 2, imag, p->dt_i, p->len2, p->inv_scale, p->k_lx,
+        p->sctab);
   } else {
     phase_field_kernel<CV><<<p->red_blocks, 256, 0, st>>>(
         (CV*)out, p->vi_dev, p->k2_dev[0], p->k2_dev[1], p->k2_dev[2], (uint32_t)p->nx_local,
         (uint32_t)p->n[1], (uint32_t)p->n[2], (uint32_t)(p->slab_r * p->nx_local), 0u, which, imag, p->dt_i,
-        p->len2, 1.0, 0);
+        p->len2, 1.0, 0, p->sctab);
   }
   return cudaGetLastError();
 }
@@ -441,6 +442,8 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
   ph.imag = p->mode == 1;
   ph.outer_off = 0;
   ph.kgen = p->kgen;
+  ph.sct = p->sctab;
+  ph.sctk = p->sctab + 256;
   ph.z_off = (uint32_t)z0;
   for (int i = 0; i < 3; ++i) {
     ph.kn[i] = (uint32_t)p->n[i];

@@ -23,6 +23,8 @@ struct PhaseArgs {
   int imag;             // imaginary time: real decay factors
   // k^2 regenerated in registers instead of loaded (kgen != 0): the plan
   // verified that (2 pi * (m * kval[a]))^2 reproduces every table entry
+  const double2* sct;   // (cos, sin)(k pi/128) for fast_sincos
+  const double2* sctk;  // the same times 1/N (the kinetic step's normalisation)
   int kgen;
   uint32_t z_off;  // global z of the pass's column 0 (z-chunked passes)
   uint32_t kn[3];
@@ -63,7 +65,7 @@ __device__ __forceinline__ void mul_vphase(CV& v, double vi, double coef, const 
     dscale(v, exp(phi));
   } else {
     double s, c;
-    fast_sincos(phi, &s, &c);
+    fast_sincos(phi, a.sct, &s, &c);
     rotate(v, c, s);
   }
 }
@@ -76,8 +78,8 @@ __device__ __forceinline__ void mul_kphase(CV& v, double kx2, double ky2, double
     dscale(v, exp(phi) * a.scale);
   } else {
     double s, c;
-    fast_sincos(phi, &s, &c);
-    rotate(v, c * a.scale, s * a.scale);
+    fast_sincos(phi, a.sctk, &s, &c);  // 1/N folded into the table
+    rotate(v, c, s);
   }
 }
 
