@@ -227,7 +227,8 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
 
 CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, void* stream) {
   if (!p || !in || !out) return fail(CTAP_EINVAL, "null argument");
-  const bool diag = kind == ctap::PASS_Y_COPY || kind == ctap::PASS_X_COPY || kind == ctap::PASS_XB_COPY;
+  const bool diag = kind == ctap::PASS_Y_COPY || kind == ctap::PASS_X_COPY || kind == ctap::PASS_XB_COPY ||
+                    kind == ctap::PASS_XP_COPY || kind == ctap::PASS_XP_KIN;
   if (!diag && (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_X_KIN_TO_PEERS))
     return fail(CTAP_EINVAL, "unknown pass %d", kind);
   const bool blk = kind >= CTAP_PASS_Y_FWD_BLK && kind <= CTAP_PASS_Y_INV_BLK;

@@ -33,6 +33,8 @@ enum PassKind {
   PASS_Y_COPY = 60,
   PASS_X_COPY = 61,
   PASS_XB_COPY = 62,
+  PASS_XP_COPY = 63,  // x-pass traffic with the x pitch padded by CTAP_XPAD points (buffer must hold it)
+  PASS_XP_KIN = 64,   // X_KIN on that padded pitch
   // strided kernel variants
   PASS_S_FWD = 100,
   PASS_S_INV = 101,

@@ -575,6 +575,18 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
         return dispatch_tile<T_COPY, false, false, false, 16>((int)nx, c64, a, tw_any, st);
       }
       return dispatch_tile<T_COPY, false, false, false>((int)nx, c64, a, tw_any, st);
+    case PASS_XP_COPY:
+    case PASS_XP_KIN: {  // diagnostics: x pass with a padded x pitch
+      static const uint32_t pad = [] {
+        const char* e = getenv("CTAP_XPAD");
+        return (uint32_t)(e ? atoi(e) : 0);
+      }();
+      a.n_outer = nyl;
+      a.lin = a.lout = Layout{NZ, 0u, nyl * NZ + pad, 0, 0u, kNone};
+      a.ph.outer_off = (uint32_t)p->slab_r * nyl;
+      if (kind == PASS_XP_COPY) return dispatch_tile<T_COPY, false, false, false>((int)nx, c64, a, tw_any, st);
+      return dispatch_tile<T_KIN, false, false, false>((int)nx, c64, a, twid(p, nx), st);
+    }
     case PASS_XB_COPY: {  // diagnostics: x-pass traffic on the x-blocked layout, block 16
       const int dlx = 4;
       const uint32_t DL = 1u << dlx;

@@ -17,7 +17,7 @@ grid = qgrid.make_grid(nx, ny, nz, (20e-6, 4e-6, 1000e-6), origin=(-10e-6, 4e-6 
 v = torch.full((nx, ny, nz), muB / 2 * 0.03, dtype=torch.float64, device="cuda")
 plan = propagator.make_plan(grid, v, species_mass("li6"), 1e-6)
 psi = torch.randn(nx, ny, nz, dtype=torch.complex128, device="cuda")
-kinds = [getattr(_lib, 'PASS_' + k) for k in (sys.argv[4].split(',') if len(sys.argv) > 4 else ['Z_MID', 'Y_FWD', 'X_KIN', 'Z_FWD', 'Z_FIRST'])]
+kinds = [int(k) if k.isdigit() else getattr(_lib, 'PASS_' + k) for k in (sys.argv[4].split(',') if len(sys.argv) > 4 else ['Z_MID', 'Y_FWD', 'X_KIN', 'Z_FWD', 'Z_FIRST'])]
 for kind in kinds:
     for _ in range(2):
         plan.native.run_pass(kind, psi, psi)
