@@ -214,9 +214,40 @@ def minima_fixtures():
     save("minima.npz", **out)
 
 
+def runner_fixtures():
+    """transverse_ground_state / initial_state of the evolve pipeline
+    (runner.py:114-181) on a 64x32x64 scaled-chip grid, and a short
+    evolution from that initial state."""
+    from ctapsim import runner
+
+    cfg = config.load_config(os.path.join(CFG, "scaled.cfg"))
+    cfg = dataclasses.replace(cfg, n_x=64, n_y=32, n_z=64)
+    layout, grid, pot, part = runner.prepare_potential(cfg)
+    iz0 = int(np.argmin(np.abs(grid.z - cfg.z_start_eff)))
+    spec = magfield.transverse_spectrum(pot, iz0, 0)
+    phi = runner.transverse_ground_state(pot, part, iz0, 0, tau=cfg.gs_tau, tol=cfg.gs_tol)
+    psi = runner.initial_state(cfg, pot, part)
+    psi0 = psi.amplitudes.copy()
+    plan = propagator.make_plan(grid, pot.values, cfg.mass, cfg.dt)
+    rec = observables.PopulationRecorder(part, stride=50, margin_cells=cfg.edge_margin_cells)
+    psi, _ = propagator.evolve_real(psi, plan, 200, [rec])
+    wires = np.array([[layout.wire_positions_at(float(z))[k] for k in ("left", "middle", "right")]
+                      for z in grid.z])
+    save("runner_scaled_64x32x64.npz", **grid_arrays(grid), xb1=part.xb1, xb2=part.xb2,
+         merged=part.merged, wire_pos=wires, iz0=iz0, phi=phi, psi0_norm=float(np.sum(np.abs(psi0) ** 2)),
+         psi0_center=psi0[:, :, iz0],
+         trace=rec.trace.as_array(), spectrum=np.array([spec.omega_x, spec.omega_y, spec.v_min,
+                                                         *spec.energies]),
+         z_start=cfg.z_start_eff, sigma_z=cfg.sigma_z_eff, gs_tau=cfg.gs_tau, gs_tol=cfg.gs_tol,
+         mass=cfg.mass, dt=cfg.dt, edge_margin=cfg.edge_margin_cells)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["minima"]:
         minima_fixtures()
+    elif sys.argv[1:] == ["runner"]:
+        runner_fixtures()
     else:
         main()
         minima_fixtures()
+        runner_fixtures()
