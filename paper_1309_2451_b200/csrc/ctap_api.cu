@@ -134,6 +134,10 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   p->kgen = 1;
   for (int i = 0; i < 3; ++i) p->kgen &= recover_kval(k2h[i], d->n[i], &p->kval[i]);
   if (const char* env = getenv("CTAP_KGEN")) p->kgen &= atoi(env) != 0;
+  // x-pass kernel of the single-GPU step: 1 warp-per-line TMA ring (default),
+  // 2 warp-per-line one tile per CTA, 0 tile_kernel (ctap_wline.cu)
+  p->wline = 1;
+  if (const char* env = getenv("CTAP_WLINE")) p->wline = atoi(env);
   p->zchunk = 0;
   if (const char* env = getenv("CTAP_ZCHUNK")) p->zchunk = atoll(env);
   if (p->zchunk % 8 || p->zchunk < 0 || (p->zchunk && d->n[2] % p->zchunk)) p->zchunk = 0;
@@ -228,7 +232,7 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
 CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, void* stream) {
   if (!p || !in || !out) return fail(CTAP_EINVAL, "null argument");
   const bool diag = kind == ctap::PASS_Y_COPY || kind == ctap::PASS_X_COPY || kind == ctap::PASS_XB_COPY ||
-                    kind == ctap::PASS_XP_COPY || kind == ctap::PASS_XP_KIN;
+                    kind == ctap::PASS_XP_COPY || kind == ctap::PASS_XP_KIN || (kind >= ctap::PASS_WX_COPY && kind <= ctap::PASS_WY_FWD);
   if (!diag && (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_X_KIN_TO_PEERS))
     return fail(CTAP_EINVAL, "unknown pass %d", kind);
   const bool blk = kind >= CTAP_PASS_Y_FWD_BLK && kind <= CTAP_PASS_Y_INV_BLK;

@@ -35,6 +35,9 @@ enum PassKind {
   PASS_XB_COPY = 62,
   PASS_XP_COPY = 63,  // x-pass traffic with the x pitch padded by CTAP_XPAD points (buffer must hold it)
   PASS_XP_KIN = 64,   // X_KIN on that padded pitch
+  PASS_WX_COPY = 65,  // warp-per-line TMA pipeline (ctap_wline.cu) without the transform, x lines
+  PASS_WY_COPY = 66,  // the same on y lines
+  PASS_WY_FWD = 67,   // forward y FFT through that pipeline
   // strided kernel variants
   PASS_S_FWD = 100,
   PASS_S_INV = 101,
@@ -56,6 +59,7 @@ struct ctap_plan {
   double* k2_dev[3];       // squared wavenumbers per axis (global lengths)
   double2* sctab;          // [256] (cos, sin)(k pi/128), [256] the same times 1/N
   int kgen;                // k^2 regenerated on device from kval (tables verified)
+  int wline;               // x-pass kernel: 1 warp-per-line ring, 2 warp-per-line tile, 0 tile_kernel
   int64_t zchunk;          // kinetic block in z chunks of this width (0: whole volume)
   double kval[3];          // 1/(n d) per axis (numpy fftfreq's val)
   int dtype;               // CTAP_C128 or CTAP_C64

@@ -391,6 +391,8 @@ cudaError_t ctap_run_phase_table(const ctap_plan* p, int which, void* out, cudaS
 // layouts, in place).  Returns a CUDA error code.
 cudaError_t ctap_run_tma_pass(const ctap_plan* p, int axis, int kind, void* data, const TileArgs& a,
                               cudaStream_t st);
+cudaError_t ctap_run_wline(const ctap_plan* p, int axis, int kind, int mode, void* data, const TileArgs& a,
+                           cudaStream_t st);
 
 static Tw twid(const ctap_plan* p, int64_t L) {
   const int off = p->tw_off[ilog2(L) - 3];
@@ -587,6 +589,15 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
       if (kind == PASS_XP_COPY) return dispatch_tile<T_COPY, false, false, false>((int)nx, c64, a, tw_any, st);
       return dispatch_tile<T_KIN, false, false, false>((int)nx, c64, a, twid(p, nx), st);
     }
+    case PASS_WX_COPY:
+    case PASS_WY_COPY:
+    case PASS_WY_FWD: {  // diagnostics: the warp-per-line TMA pipeline on x / y lines
+      if (in != out) return cudaErrorInvalidValue;
+      const bool xa = kind == PASS_WX_COPY;
+      a.n_outer = xa ? nyl : nxl;
+      a.ph.outer_off = xa ? (uint32_t)p->slab_r * nyl : 0u;
+      return ctap_run_wline(p, xa ? 2 : 1, kind == PASS_WY_FWD ? T_FWD : T_COPY, p->wline == 2 ? 2 : 1, out, a, st);
+    }
     case PASS_XB_COPY: {  // diagnostics: x-pass traffic on the x-blocked layout, block 16
       const int dlx = 4;
       const uint32_t DL = 1u << dlx;
@@ -605,6 +616,12 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
       a.ph.outer_off = (uint32_t)p->slab_r * nyl;
       const Tw tw = twid(p, nx);
       const int L = (int)nx;
+      if (kind == PASS_X_KIN && !c64 && !zsub && in == out && !p->expk_dev) {
+        // warp-per-line TMA pipeline (ctap_wline.cu): the default complex128 x pass
+        const int tk = kind == PASS_X_KIN ? T_KIN : kind == PASS_X_FWD ? T_FWD : T_INV;
+        cudaError_t e = ctap_run_wline(p, 2, tk, p->wline, out, a, st);
+        if (e != cudaErrorNotSupported) return e;
+      }
       if (use_tma_x && in == out && !(kind == PASS_X_KIN && p->expk_dev)) {
         const int tk = kind == PASS_X_KIN ? T_KIN : kind == PASS_X_FWD ? T_FWD : T_INV;
         cudaError_t e = ctap_run_tma_pass(p, 2, tk, out, a, st);

@@ -1,0 +1,396 @@
+// Warp-per-line strided passes (complex128): the [x K x^-1] sweep of the
+// single-GPU step and the plain x (and, for diagnostics, y) FFT passes.
+//
+// Reference: propagator.py:98-107 (_advance) -- forward x FFT,
+// exp(-i k^2 dt/2)/N, inverse x FFT of one telescoped step -- and the x FFTs
+// of the 3D transform (ctap_fft3d).
+//
+// Why a second strided kernel: tile_kernel (ctap_passes.cu) spreads each
+// 512-point column over 64 threads of a 512-thread block, so every radix
+// exchange is a 16-warp __syncthreads; the x pass measured 1.43 ms at 512^3
+// with the FP64 pipe ~40 % and DRAM ~34 % busy.  Here ONE WARP OWNS ONE
+// COLUMN (E = L/32 points per lane, L = 256 or 512):
+//   * every FFT exchange is warp-private, in place in the column's own slots
+//     of the shared tile, synchronised by __syncwarp only;
+//   * the tile is stored with a 128-byte XOR swizzle (element i of column c in
+//     row i, 16-byte chunk c ^ (i & 7)) and the exchange index is further
+//     permuted by sigma(e) = e ^ ((e >> 3) & 7), which makes the column reads
+//     and every radix-8 scatter/gather bank-conflict free;
+//   * the kinetic factor is symmetric in kx (k^2 of index i and L - i are
+//     bitwise equal) and the mirror of lane t's point t + 32 m is held by lane
+//     32 - t of the same warp: each lane evaluates the exact phase and its
+//     sincos for half of its points and receives the other half by shuffle.
+// Two tile movers (plan->wline, env CTAP_WLINE; DESIGN.md §4 has the measurements):
+//   1 (ring)  persistent CTA per SM, 2 compute groups of 8 warps, a ring of 3
+//             tile buffers filled and drained by TMA (cp.async.bulk.tensor,
+//             hardware 128-byte swizzle); the last warp to finish a tile
+//             stores it and refills the buffer;
+//   2 (tile)  one tile per 256-thread CTA, 2 CTAs per SM, rows moved through
+//             registers with coalesced 16-byte loads/stores (as tile_kernel).
+// Arithmetic is identical to tile_kernel's (same radix plan and twiddles, same
+// phase recipe and rotation), so the kernels are bitwise interchangeable
+// (tests/test_gpu_parity.py::test_wline_bitwise_equals_tile_kernel).
+#include <cuda.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "ctap_device.cuh"
+#include "ctap_internal.h"
+#include "ctap_tile.cuh"
+
+namespace ctap {
+namespace wl {
+
+constexpr int kCols = 8;    // columns (lines) per tile, one warp each
+#ifndef CTAP_WL_GROUPS
+#define CTAP_WL_GROUPS 2
+#endif
+constexpr int kGroups = CTAP_WL_GROUPS;  // ring: tiles in computation at once
+constexpr int kBufs = 3;    // ring: tile buffers
+constexpr int kRingThreads = kGroups * kCols * 32;  // 2 groups: 16 warps, 4 per SM sub-partition, 128 registers each
+constexpr int kTileThreads = kCols * 32;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WL_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WL_WAIT_%=;\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Column c of a [row][8] complex128 tile with the 128-byte XOR swizzle
+// (identical to TMA's CU_TENSOR_MAP_SWIZZLE_128B on a 1 KB aligned buffer).
+struct SwzCol {
+  double2* buf;
+  int c;
+  __device__ __forceinline__ double2& nat(int i) const { return buf[i * 8 + (c ^ (i & 7))]; }
+  __device__ __forceinline__ double2& at(int e) const { return nat(e ^ ((e >> 3) & 7)); }
+};
+
+// exp(-i k^2 dt/2)/N (real time: (cos, sin); imaginary time: (decay, 0)),
+// the recipe of mul_kphase (ctap_tile.cuh)
+__device__ __forceinline__ double2 kfactor(double kx2, double ky2, double kz2, const PhaseArgs& a) {
+  const double phi = k_phase(kx2, ky2, kz2, a.len2, a.dt_i);
+  if (a.imag) return make_double2(exp(phi) * a.scale, 0.0);
+  double s, c;
+  fast_sincos(phi, a.sctk, &s, &c);
+  return make_double2(c, s);
+}
+__device__ __forceinline__ void apply_k(double2& v, double2 f, int imag) {
+  if (imag) dscale(v, f.x);
+  else rotate(v, f.x, f.y);
+}
+__device__ __forceinline__ double kx2_of(uint32_t i, const PhaseArgs& a) {
+  return a.kgen ? k2_gen(i, a.kn[0], a.kval[0]) : __ldg(&a.kx2[i]);
+}
+__device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+// The warp's column: read (natural order), transform, write back.  o = outer
+// index (y of the x pass), z = the column's global z.
+template <int L, int KIND>
+__device__ __forceinline__ void column(const SwzCol& col, int lane, const double2* __restrict__ tw,
+                                       const PhaseArgs& ph, uint32_t o, uint32_t z) {
+  constexpr int E = L / 32;
+  double2 v[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) v[m] = col.nat(lane + 32 * m);
+  __syncwarp();
+  if constexpr (KIND == T_COPY) {  // diagnostics: the tile mover alone
+  } else if constexpr (KIND == T_FWD) {
+    line_fft<L, -1, E>(v, lane, tw, col, SyncWarp{});
+  } else if constexpr (KIND == T_INV) {
+    line_fft<L, +1, E>(v, lane, tw, col, SyncWarp{});
+  } else {  // T_KIN
+    double ky2, kz2;
+    if (ph.kgen) {
+      ky2 = k2_gen(ph.outer_off + o, ph.kn[1], ph.kval[1]);
+      kz2 = k2_gen(ph.z_off + z, ph.kn[2], ph.kval[2]);
+    } else {
+      ky2 = __ldg(&ph.ky2[ph.outer_off + o]);
+      kz2 = __ldg(&ph.kz2[ph.z_off + z]);
+    }
+    line_fft<L, -1, E>(v, lane, tw, col, SyncWarp{});
+    // Lane t evaluates the factor of its point t + 32 q (q < E/2, index <
+    // L/2).  Its point m = E - q has index L - ((32 - t) + 32 (q - 1)), the
+    // mirror of lane 32 - t's point of iteration q - 1, received by shuffle;
+    // lane 0 (indices 32 m, self-mirrored at 0 and L/2) uses its own factor of
+    // index 32 q for m = E - q and evaluates index L/2 at the end.
+    const int mirror = (32 - lane) & 31;
+    double2 shp = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < E / 2; ++q) {
+      const double2 f = kfactor(kx2_of(lane + 32 * q, ph), ky2, kz2, ph);
+      apply_k(v[q], f, ph.imag);
+      if (q >= 1) apply_k(v[E - q], lane == 0 ? f : shp, ph.imag);
+      shp = shfl2(f, mirror);
+    }
+    const double2 fn = kfactor(kx2_of(L / 2, ph), ky2, kz2, ph);
+    apply_k(v[E / 2], lane == 0 ? fn : shp, ph.imag);
+    line_fft<L, +1, E>(v, lane, tw, col, SyncWarp{});
+  }
+#pragma unroll
+  for (int m = 0; m < E; ++m) col.nat(lane + 32 * m) = v[m];
+}
+
+// ---------------------------------------------------------------------------
+// mover 1: persistent TMA ring
+// ---------------------------------------------------------------------------
+template <int L, int KIND, int AXIS>
+__global__ void __launch_bounds__(kRingThreads, 1)
+    ring_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a, const double2* __restrict__ tw) {
+  constexpr int BOX = L < 256 ? L : 256;
+  constexpr uint32_t kTileBytes = (uint32_t)L * kCols * sizeof(double2);
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // swizzle atom: 1 KB
+  double2* bufs = reinterpret_cast<double2*>(base);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + kBufs * kTileBytes);
+  uint64_t* done = full + kBufs;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(done + kBufs);  // columns finished per fill
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ntiles = a.n_outer * a.nchunk;
+  const uint32_t nloc = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto coords = [&](uint32_t j, int& c0, int& o) {
+    const uint32_t tile = blockIdx.x + j * gridDim.x;
+    const uint32_t oo = tile / a.nchunk;
+    c0 = (int)((tile - oo * a.nchunk) * 16);  // 8 complex = 16 scalars per column block
+    o = (int)oo;
+  };
+  auto load = [&](uint32_t j) {
+    const int b = j % kBufs;
+    double2* buf = bufs + (size_t)b * L * kCols;
+    int c0, o;
+    coords(j, c0, o);
+    fence_async_smem();
+    bar_expect_tx(&full[b], kTileBytes);
+#pragma unroll
+    for (int q = 0; q < L / BOX; ++q)
+      tma_load(buf + q * BOX * kCols, &tmap, &full[b], c0, AXIS == 2 ? o : q * BOX, AXIS == 2 ? q * BOX : o);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kBufs; ++b) {
+      bar_init(&full[b], 1);
+      bar_init(&done[b], kCols);
+      cnt[b] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (uint32_t j = 0; j < (uint32_t)kBufs && j < nloc; ++j) load(j);
+  }
+  __syncthreads();
+
+  const int g = warp / kCols, c = warp % kCols;
+  for (uint32_t j = g; j < nloc; j += kGroups) {
+    const int b = j % kBufs;
+    const uint32_t k = j / kBufs;
+    // fill k - 1 of this buffer (the other group's tile) must be consumed
+    // before waiting on fill k, or the full-barrier parity would alias
+    if (k >= 1) bar_wait(&done[b], (k - 1) & 1);
+    bar_wait(&full[b], k & 1);
+    const uint32_t tile = blockIdx.x + j * gridDim.x;
+    const uint32_t o = tile / a.nchunk;
+    const uint32_t z = (tile - o * a.nchunk) * 8 + c;
+    double2* buf = bufs + (size_t)b * L * kCols;
+    column<L, KIND>(SwzCol{buf, c}, lane, tw, a.ph, o, z);
+    fence_async_smem();  // generic-proxy writes -> the TMA store
+    __syncwarp();
+    if (lane == 0) {
+      // the last of the tile's 8 warps writes it back and refills the buffer
+      // with tile j + kBufs (a dedicated producer warp would make 17 warps and
+      // cap the registers at 96 per thread)
+      __threadfence_block();
+      const bool last = atomicAdd(&cnt[b], 1u) == kCols - 1;
+      __threadfence_block();
+      bar_arrive(&done[b]);
+      if (last) {
+        cnt[b] = 0;
+        int c0, oo;
+        coords(j, c0, oo);
+#pragma unroll
+        for (int q = 0; q < L / BOX; ++q)
+          tma_store(&tmap, buf + q * BOX * kCols, c0, AXIS == 2 ? oo : q * BOX, AXIS == 2 ? q * BOX : oo);
+        bulk_commit();
+        bulk_wait_read0();  // the buffer may be refilled once the store has read it
+        if (j + kBufs < nloc) load(j + kBufs);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// mover 2: one tile per CTA, rows through registers
+// ---------------------------------------------------------------------------
+struct Strides {
+  uint32_t rs, os;  // row (line-axis) and outer strides, in complex elements
+};
+
+template <int L, int KIND>
+__global__ void __launch_bounds__(kTileThreads, 2)
+    tile1_kernel(double2* __restrict__ psi, Strides s, TileArgs a, const double2* __restrict__ tw) {
+  constexpr int kMoves = L / kCols / 4;  // 16-byte moves per lane (8 lanes per 128-byte row)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t tile = blockIdx.x;
+  const uint32_t o = tile / a.nchunk;
+  const uint32_t zc = tile - o * a.nchunk;
+  double2* g = psi + o * s.os + zc * 8 + (lane & 7);
+  const int row0 = warp * (L / kCols) + (lane >> 3), ch = lane & 7;
+  {
+    double2 r[kMoves];
+#pragma unroll
+    for (int q = 0; q < kMoves; ++q) r[q] = __ldcg(g + (size_t)(row0 + 4 * q) * s.rs);
+#pragma unroll
+    for (int q = 0; q < kMoves; ++q) {
+      const int row = row0 + 4 * q;
+      buf[row * 8 + (ch ^ (row & 7))] = r[q];
+    }
+  }
+  __syncthreads();
+  column<L, KIND>(SwzCol{buf, warp}, lane, tw, a.ph, o, zc * 8 + warp);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kMoves; ++q) {
+    const int row = row0 + 4 * q;
+    __stcg(g + (size_t)row * s.rs, buf[row * 8 + (ch ^ (row & 7))]);
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return (EncodeTiledFn)p;
+  }();
+  return fn;
+}
+
+static int sm_count() {
+  static int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return sms;
+}
+
+// AXIS 2: x lines of an (L, n_outer, nz) array; AXIS 1: y lines of an
+// (n_outer, L, nz) array (nz = 8 * a.nchunk)
+template <int L, int KIND, int AXIS>
+static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw, cudaStream_t st) {
+  constexpr int BOX = L < 256 ? L : 256;
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  const uint64_t nz2 = (uint64_t)a.nchunk * 8 * 2;  // scalars per z line
+  const uint64_t d1 = AXIS == 2 ? a.n_outer : L, d2 = AXIS == 2 ? L : a.n_outer;
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof map);
+  const cuuint64_t dims[3] = {nz2, d1, d2};
+  const cuuint64_t strides[2] = {nz2 * sizeof(double), nz2 * sizeof(double) * d1};
+  const cuuint32_t box[3] = {16, AXIS == 2 ? 1u : (cuuint32_t)BOX, AXIS == 2 ? (cuuint32_t)BOX : 1u};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, data, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  auto k = ring_kernel<L, KIND, AXIS>;
+  constexpr size_t smem =
+      (size_t)kBufs * L * kCols * sizeof(double2) + 2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t) + 1024;
+  static cudaError_t init = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (init != cudaSuccess) return init;
+  const uint32_t ntiles = a.n_outer * a.nchunk;
+  const uint32_t grid = ntiles < (uint32_t)sm_count() ? ntiles : (uint32_t)sm_count();
+  k<<<grid, kRingThreads, smem, st>>>(map, a, tw);
+  return cudaGetLastError();
+}
+
+template <int L, int KIND, int AXIS>
+static cudaError_t launch_tile1(const TileArgs& a, void* data, const double2* tw, cudaStream_t st) {
+  const uint32_t nz = a.nchunk * 8;
+  Strides s;
+  s.rs = AXIS == 2 ? a.n_outer * nz : nz;
+  s.os = AXIS == 2 ? nz : (uint32_t)L * nz;
+  auto k = tile1_kernel<L, KIND>;
+  constexpr size_t smem = (size_t)L * kCols * sizeof(double2);
+  static cudaError_t init = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (init != cudaSuccess) return init;
+  k<<<a.n_outer * a.nchunk, kTileThreads, smem, st>>>((double2*)data, s, a, tw);
+  return cudaGetLastError();
+}
+
+}  // namespace wl
+}  // namespace ctap
+
+using namespace ctap;
+
+// In-place strided pass on lines of length L = 256 or 512 through the
+// warp-per-line kernels: axis 2 = x lines of an (L, n_outer, nz) array
+// (kinds T_FWD, T_INV, T_KIN, T_COPY), axis 1 = y lines of an (n_outer, L, nz)
+// array (T_FWD, T_INV, T_COPY).  `mode` 1 ring, 2 tile; returns
+// cudaErrorNotSupported outside these shapes (the caller then uses tile_kernel).
+cudaError_t ctap_run_wline(const ctap_plan* p, int axis, int kind, int mode, void* data, const TileArgs& a,
+                           cudaStream_t st) {
+  if (p->dtype != CTAP_C128 || mode < 1 || mode > 2) return cudaErrorNotSupported;
+  const int64_t L = axis == 2 ? p->n[0] : p->n[1];
+  if (L != 256 && L != 512) return cudaErrorNotSupported;
+  if (axis == 1 && kind == T_KIN) return cudaErrorNotSupported;
+  const double2* tw = p->twiddles + p->tw_off[L == 256 ? 5 : 6];
+#define CTAP_WL_K(LL, KK, AX) \
+  (mode == 1 ? wl::launch_ring<LL, KK, AX>(a, data, tw, st) : wl::launch_tile1<LL, KK, AX>(a, data, tw, st))
+#define CTAP_WL(LL, AX)                          \
+  switch (kind) {                                \
+    case T_FWD: return CTAP_WL_K(LL, T_FWD, AX); \
+    case T_INV: return CTAP_WL_K(LL, T_INV, AX); \
+    case T_COPY: return CTAP_WL_K(LL, T_COPY, AX); \
+  }                                              \
+  return cudaErrorNotSupported;
+  if (axis == 2) {
+    if (kind == T_KIN) return L == 512 ? CTAP_WL_K(512, T_KIN, 2) : CTAP_WL_K(256, T_KIN, 2);
+    if (L == 512) { CTAP_WL(512, 2) }
+    CTAP_WL(256, 2)
+  }
+  if (L == 512) { CTAP_WL(512, 1) }
+  CTAP_WL(256, 1)
+#undef CTAP_WL
+#undef CTAP_WL_K
+}

@@ -32,7 +32,7 @@ def main():
               ("Y_INV", P.PASS_Y_INV, 32), ("Z_FIRST", P.PASS_Z_FIRST, 40), ("Z_LAST", P.PASS_Z_LAST, 40),
               ("Z_FWD", P.PASS_Z_FWD, 32), ("X_FWD", P.PASS_X_FWD, 32), ("X_INV", P.PASS_X_INV, 32)]
     kbuf = torch.empty_like(psi)
-    passes += [("Y_COPY", 60, 32), ("X_COPY", 61, 32), ("XB_COPY", 62, 32)]
+    passes += [("Y_COPY", 60, 32), ("X_COPY", 61, 32), ("XB_COPY", 62, 32), ("WX_COPY", 65, 32), ("WY_COPY", 66, 32), ("WY_FWD", 67, 32)]
     io = {P.PASS_Y_FWD_BLK: (psi, kbuf), P.PASS_X_KIN_BLK: (kbuf, kbuf), P.PASS_Y_INV_BLK: (kbuf, psi)}
     total = 0.0
     for name, kind, bpp in passes:
