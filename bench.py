@@ -283,6 +283,12 @@ def run_ours(args):
         plan = propagator.make_plan(grid, v_local, m, DT, phase_tables=tables)
         part = observables.symmetric_partition(grid, 3.5e-6)
         stride = max(1, args.steps // 4)
+        # one untimed warm-up call of the same path (pinned staging buffers,
+        # graph capture) -- the timed call is the steady-state user call
+        wu = qgrid.Wavefunction(host.numpy().copy(), grid)
+        wu, _ = propagator.evolve_real(wu, plan, 2, [observables.PopulationRecorder(part, stride=1)])
+        _ = wu.amplitudes
+        del wu, _
         rec = observables.PopulationRecorder(part, stride=stride)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
