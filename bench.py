@@ -402,9 +402,11 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": val, "unit": "steps/s", "n_gpus": args.gpus, "steps": k,
         "warmup": args.warmup, "ms_per_step": 1000.0 / val, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "complex128", "data": "synthetic: run_bench harmonic trap, Gaussian packet",
-        "config": {"workload": "512^3 split-step propagation, complex128, dt = 1 us, Li-6 (BASELINE config 4)",
-                   "grid": list(GRID_N)},
+        "vs_baseline": None, "dtype": "complex128",
+        "data": "synthetic: Gaussian packet; V = the run_bench harmonic field of the same shape (the split step's "
+                "cost does not depend on V's values; the paper-chip V takes ~66 min of host numba at 512^3)",
+        "config": {"workload": "512^3 CTAP split-step propagation, complex128, dt = 1 us, Li-6 (BASELINE config 4)",
+                   "grid": list(GRID_N), "extents_m": list(EXTENTS), "decomposition": "host threads"},
         "impl": "reference",
         "cpu_baseline": {"value": val, "unit": "steps/s", "cores": cores, "kind": "port",
                          "sample": f"{k} telescoped split steps of the full 512^3 grid on {cores} host threads "
