@@ -393,6 +393,7 @@ cudaError_t ctap_run_tma_pass(const ctap_plan* p, int axis, int kind, void* data
                               cudaStream_t st);
 cudaError_t ctap_run_wline(const ctap_plan* p, int axis, int kind, int mode, void* data, const TileArgs& a,
                            cudaStream_t st);
+cudaError_t ctap_run_wline_peers(const ctap_plan* p, const void* in, const TileArgs& a, cudaStream_t st);
 
 static Tw twid(const ctap_plan* p, int64_t L) {
   const int off = p->tw_off[ilog2(L) - 3];
@@ -513,6 +514,10 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
       a.ph.outer_off = (uint32_t)p->slab_r * nyl;
       for (int q = 0; q < P; ++q)
         a.peers[q] = (char*)p->peer_p[q] + csz * (size_t)p->slab_r * nxl * nyl * NZ;
+      if (!zsub && !p->expk_dev) {  // warp-per-line ring, TMA stores into the peers (ctap_wline.cu)
+        cudaError_t e = ctap_run_wline_peers(p, a.in, a, st);
+        if (e != cudaErrorNotSupported) return e;
+      }
       return dispatch_tile<T_KIN, false, true, false, 8, true>((int)nx, c64, a, twid(p, nx), st);
     }
     case PASS_Y_FWD_BLK:

@@ -87,6 +87,7 @@ __device__ __forceinline__ void tma_store(const CUtensorMap* map, const void* sr
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Column c of a [row][8] complex128 tile with the 128-byte XOR swizzle
@@ -168,9 +169,22 @@ __device__ __forceinline__ void column(const SwzCol& col, int lane, const double
 // ---------------------------------------------------------------------------
 // mover 1: persistent TMA ring
 // ---------------------------------------------------------------------------
-template <int L, int KIND, int AXIS>
+// Destinations of the fused slab transpose (AXIS 4): rows [q nxl, (q+1) nxl)
+// of every x tile go to rank q's peer-major buffer, through one tensor map per
+// rank over that (peer-mapped, NVLink) buffer.
+struct PeerMaps {
+  CUtensorMap m[kMaxRanks];
+  int P;
+};
+struct NoPeers {};
+
+// AXIS 1 / 2: y / x lines of the natural layout (in place); AXIS 4: x lines of
+// the slab's y-slab, results stored by TMA straight into the other ranks'
+// buffers (the transpose of the fused slab transport).
+template <int L, int KIND, int AXIS, typename PM>
 __global__ void __launch_bounds__(kRingThreads, 1)
-    ring_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a, const double2* __restrict__ tw) {
+    ring_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a, const double2* __restrict__ tw,
+                const __grid_constant__ PM pm) {
   constexpr int BOX = L < 256 ? L : 256;
   constexpr uint32_t kTileBytes = (uint32_t)L * kCols * sizeof(double2);
   extern __shared__ unsigned char smem_raw[];
@@ -197,7 +211,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
     bar_expect_tx(&full[b], kTileBytes);
 #pragma unroll
     for (int q = 0; q < L / BOX; ++q)
-      tma_load(buf + q * BOX * kCols, &tmap, &full[b], c0, AXIS == 2 ? o : q * BOX, AXIS == 2 ? q * BOX : o);
+      tma_load(buf + q * BOX * kCols, &tmap, &full[b], c0, AXIS != 1 ? o : q * BOX, AXIS != 1 ? q * BOX : o);
   };
 
   if (threadIdx.x == 0) {
@@ -238,14 +252,24 @@ __global__ void __launch_bounds__(kRingThreads, 1)
         cnt[b] = 0;
         int c0, oo;
         coords(j, c0, oo);
+        if constexpr (AXIS == 4) {
+          const int nxl = L / pm.P, bx = nxl < BOX ? nxl : BOX;
+          for (int q = 0; q < pm.P; ++q)
+            for (int r0 = 0; r0 < nxl; r0 += bx) tma_store(&pm.m[q], buf + (q * nxl + r0) * kCols, c0, oo, r0);
+        } else {
 #pragma unroll
-        for (int q = 0; q < L / BOX; ++q)
-          tma_store(&tmap, buf + q * BOX * kCols, c0, AXIS == 2 ? oo : q * BOX, AXIS == 2 ? q * BOX : oo);
+          for (int q = 0; q < L / BOX; ++q)
+            tma_store(&tmap, buf + q * BOX * kCols, c0, AXIS == 2 ? oo : q * BOX, AXIS == 2 ? q * BOX : oo);
+        }
         bulk_commit();
         bulk_wait_read0();  // the buffer may be refilled once the store has read it
         if (j + kBufs < nloc) load(j + kBufs);
       }
     }
+  }
+  if (lane == 0) {
+    bulk_wait0();  // this thread's bulk stores are complete (no-op if it issued none)
+    if constexpr (AXIS == 4) __threadfence_system();
   }
 }
 
@@ -333,14 +357,59 @@ static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  auto k = ring_kernel<L, KIND, AXIS>;
+  auto k = ring_kernel<L, KIND, AXIS, NoPeers>;
   constexpr size_t smem =
       (size_t)kBufs * L * kCols * sizeof(double2) + 2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t) + 1024;
   static cudaError_t init = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (init != cudaSuccess) return init;
   const uint32_t ntiles = a.n_outer * a.nchunk;
   const uint32_t grid = ntiles < (uint32_t)sm_count() ? ntiles : (uint32_t)sm_count();
-  k<<<grid, kRingThreads, smem, st>>>(map, a, tw);
+  k<<<grid, kRingThreads, smem, st>>>(map, a, tw, NoPeers{});
+  return cudaGetLastError();
+}
+
+// [x K x^-1] of the y-slab (L = nx, n_outer = ny/P, nz) with the fused
+// transpose: tile rows of rank q's x range are TMA-stored into a.peers[q]
+// (peer-major (nx/P, ny/P, nz) block of this rank inside rank q's buffer).
+template <int L>
+static cudaError_t launch_ring_peers(const TileArgs& a, const void* in, int P, const double2* tw, cudaStream_t st) {
+  constexpr int BOX = L < 256 ? L : 256;
+  EncodeTiledFn enc = encode_fn();
+  if (!enc || P < 2 || P > kMaxRanks || L % P) return cudaErrorNotSupported;
+  const uint64_t nz2 = (uint64_t)a.nchunk * 8 * 2;
+  const uint64_t nxl = L / P;
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof map);
+  {
+    const cuuint64_t dims[3] = {nz2, a.n_outer, (cuuint64_t)L};
+    const cuuint64_t strides[2] = {nz2 * sizeof(double), nz2 * sizeof(double) * a.n_outer};
+    const cuuint32_t box[3] = {16, 1, (cuuint32_t)BOX};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(in), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  PeerMaps pm;
+  std::memset(&pm, 0, sizeof pm);
+  pm.P = P;
+  for (int q = 0; q < P; ++q) {
+    const cuuint64_t dims[3] = {nz2, a.n_outer, nxl};
+    const cuuint64_t strides[2] = {nz2 * sizeof(double), nz2 * sizeof(double) * a.n_outer};
+    const cuuint32_t box[3] = {16, 1, (cuuint32_t)(nxl < (uint64_t)BOX ? nxl : BOX)};
+    if (enc(&pm.m[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.peers[q], dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  auto k = ring_kernel<L, T_KIN, 4, PeerMaps>;
+  constexpr size_t smem =
+      (size_t)kBufs * L * kCols * sizeof(double2) + 2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t) + 1024;
+  static cudaError_t init = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (init != cudaSuccess) return init;
+  const uint32_t ntiles = a.n_outer * a.nchunk;
+  const uint32_t grid = ntiles < (uint32_t)sm_count() ? ntiles : (uint32_t)sm_count();
+  k<<<grid, kRingThreads, smem, st>>>(map, a, tw, pm);
   return cudaGetLastError();
 }
 
@@ -393,4 +462,16 @@ cudaError_t ctap_run_wline(const ctap_plan* p, int axis, int kind, int mode, voi
   CTAP_WL(256, 1)
 #undef CTAP_WL
 #undef CTAP_WL_K
+}
+
+// The fused slab transport's [x K x^-1] (PASS_X_KIN_TO_PEERS) through the ring
+// with per-rank TMA stores; cudaErrorNotSupported outside complex128,
+// nx = 256 / 512 (the caller then uses tile_kernel's peer stores).
+cudaError_t ctap_run_wline_peers(const ctap_plan* p, const void* in, const TileArgs& a, cudaStream_t st) {
+  if (p->dtype != CTAP_C128 || p->wline != 1) return cudaErrorNotSupported;
+  const int64_t L = p->n[0];
+  const double2* tw = p->twiddles + p->tw_off[L == 256 ? 5 : 6];
+  if (L == 512) return wl::launch_ring_peers<512>(a, in, p->slab_p, tw, st);
+  if (L == 256) return wl::launch_ring_peers<256>(a, in, p->slab_p, tw, st);
+  return cudaErrorNotSupported;
 }

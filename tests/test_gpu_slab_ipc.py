@@ -25,12 +25,12 @@ def _port():
         return s.getsockname()[1]
 
 
-def _case():
+def _case(n=(32, 16, 32)):
     from paper_1309_2451_b200 import qgrid
     from paper_1309_2451_b200.constants import muB, species_mass
 
     m = species_mass("li6")
-    grid = qgrid.make_grid(32, 16, 32, (20e-6, 4e-6, 250e-6), origin=(-10e-6, 4e-6 / 32, 0.0))
+    grid = qgrid.make_grid(*n, (20e-6, 4e-6, 250e-6), origin=(-10e-6, 4e-6 / n[1] / 2, 0.0))
     om = 2 * np.pi * np.array([2e3, 2e4, 20.0])
     x, y, z = grid.meshgrid()
     v = muB / 2 * 0.03 + 0.5 * m * (om[0] ** 2 * x ** 2 + om[1] ** 2 * (y - 2e-6) ** 2
@@ -40,7 +40,7 @@ def _case():
     return grid, v, a0, m
 
 
-def _worker(rank, world, port, steps, out):
+def _worker(rank, world, port, steps, out, n):
     here = os.path.dirname(os.path.abspath(__file__))
     for p in (here, os.path.dirname(here)):
         if p not in sys.path:
@@ -51,7 +51,7 @@ def _worker(rank, world, port, steps, out):
     try:
         from paper_1309_2451_b200 import slab
 
-        grid, v, a0, m = _case()
+        grid, v, a0, m = _case(n)
         lay = slab.SlabLayout(grid.n, world, rank)
 
         def barrier():
@@ -71,14 +71,16 @@ def _worker(rank, world, port, steps, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_fused_ipc_two_processes_bitwise(tmp_path, world):
+@pytest.mark.parametrize("world,n", [(2, (32, 16, 32)), (2, (256, 16, 16))])
+def test_fused_ipc_two_processes_bitwise(tmp_path, world, n):
+    """n = (256, ...) runs the x pass through the warp-per-line ring, whose TMA
+    stores then target the other process's IPC-mapped buffer."""
     from paper_1309_2451_b200 import propagator, qgrid
 
     out = str(tmp_path / "psi")
-    mp.spawn(_worker, args=(world, _port(), 5, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _port(), 5, out, n), nprocs=world, join=True)
     got = np.concatenate([np.load(f"{out}.{r}.npy") for r in range(world)])
-    grid, v, a0, m = _case()
+    grid, v, a0, m = _case(n)
     psi = qgrid.Wavefunction(a0.copy(), grid)
     psi, _ = propagator.evolve_real(psi, propagator.make_plan(grid, v, m, 1e-6, phase_tables=0), 5)
     assert np.array_equal(got, psi.amplitudes)

@@ -54,9 +54,10 @@ def run_virtual(grid, v, a0, P, steps, tables=0):
     return out.cpu().numpy(), plans, bufs, lays
 
 
-@pytest.mark.parametrize("P,tables", [(2, 0), (4, 0), (8, 0), (2, 1), (4, 3)])
-def test_virtual_slabs_bitwise_equal_single_gpu(P, tables):
-    grid, v, a0 = _case()
+@pytest.mark.parametrize("P,tables,n", [(2, 0, (32, 16, 32)), (4, 0, (32, 16, 32)), (8, 0, (32, 16, 32)),
+                                         (2, 1, (32, 16, 32)), (4, 3, (32, 16, 32)), (4, 0, (256, 16, 16))])
+def test_virtual_slabs_bitwise_equal_single_gpu(P, tables, n):
+    grid, v, a0 = _case(n)
     got, *_ = run_virtual(grid, v, a0, P, 6, tables)
     psi = qgrid.Wavefunction(a0.copy(), grid)
     plan = propagator.make_plan(grid, v, M, 1e-6, phase_tables=tables)
@@ -130,9 +131,12 @@ def run_virtual_fused(grid, v, a0, P, steps, tables=0):
     return torch.cat(psi).reshape(grid.n).cpu().numpy()
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
-def test_fused_transport_bitwise_equal_single_gpu(P):
-    grid, v, a0 = _case()
+@pytest.mark.parametrize("P,n", [(2, (32, 16, 32)), (4, (32, 16, 32)), (8, (32, 16, 32)),
+                                 (2, (256, 16, 16)), (8, (256, 16, 16)), (4, (512, 8, 16))])
+def test_fused_transport_bitwise_equal_single_gpu(P, n):
+    """nx = 256 / 512 run the x pass through the warp-per-line ring with TMA
+    stores into the peers' buffers; smaller nx through tile_kernel's peer stores."""
+    grid, v, a0 = _case(n)
     got = run_virtual_fused(grid, v, a0, P, 6)
     psi = qgrid.Wavefunction(a0.copy(), grid)
     plan = propagator.make_plan(grid, v, M, 1e-6, phase_tables=0)
