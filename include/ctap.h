@@ -76,8 +76,23 @@ typedef enum ctap_pass_kind {
    * (peer memory over NVLink) registered with ctap_set_peer_buffers; the
    * caller inserts a stream-ordered cross-rank barrier after each. */
   CTAP_PASS_Y_FWD_TO_PEERS = 15, /* in: psi x-slab; out: every rank's y-slab buffer */
-  CTAP_PASS_X_KIN_TO_PEERS = 16  /* in: this rank's y-slab buffer; out: every rank's
+  CTAP_PASS_X_KIN_TO_PEERS = 16, /* in: this rank's y-slab buffer; out: every rank's
                                     peer-major buffer (then CTAP_PASS_Y_INV_FROM_PEER) */
+  /* pencil decomposition (ctap_plan_desc.pencil_c > 1; Pr x Pc ranks, rank
+   * r = a Pc + b owns x block a (nx/Pr), y block b (ny/Pc), all z).  Buffers:
+   *   psi  natural (nx/Pr, ny/Pc, nz)                       position space
+   *   Zc   [b'][x][y][z'] (z chunk b' of nz/Pc)            = send of the row all-to-all
+   *   Yb   [b'][x][y'][z'] (y block b' of ny/Pc)           = receive of the row all-to-all
+   *   Xp   [a'][x][y'][z'] (y block a' of ny/Pr)           = send of the column all-to-all
+   *   Xr   [a'][x'][y][z'] = natural (nx, ny/Pr, nz/Pc)    = receive of the column all-to-all
+   * One step: PZ_MID (Zc) -> row a2a -> PY_FWD (Yb -> Xp) -> column a2a ->
+   * PX_KIN (Xr) -> column a2a -> PY_INV (Xp -> Yb) -> row a2a. */
+  CTAP_PASS_PZ_FIRST = 17, /* Fz Vh: psi (natural) -> Zc, out of place */
+  CTAP_PASS_PZ_MID = 18,   /* Fz V Fz^-1 on Zc, in place */
+  CTAP_PASS_PZ_LAST = 19,  /* Vh Fz^-1: Zc -> psi (natural), out of place */
+  CTAP_PASS_PY_FWD = 20,   /* Fy: Yb -> Xp */
+  CTAP_PASS_PY_INV = 21,   /* Fy^-1: Xp -> Yb */
+  CTAP_PASS_PX_KIN = 22    /* Fx^-1 (K/N) Fx on Xr, in place */
 } ctap_pass_kind;
 
 typedef struct ctap_plan ctap_plan;
@@ -104,7 +119,9 @@ typedef struct ctap_plan_desc {
                            step.  All variants use the identical phase
                            arithmetic (real time only; ignored otherwise). */
   int32_t dtype;    /* ctap_dtype of every wavefunction buffer passed to the plan */
-  int32_t reserved;
+  int32_t pencil_c; /* 0 or 1: x slabs over slab_p ranks; Pc > 1: the slab_p ranks form a
+                       (slab_p / Pc) x Pc pencil grid over (x, y), slab_r = a Pc + b; the
+                       potential (and psi) is then the (nx/Pr, ny/Pc, nz) block */
 } ctap_plan_desc;
 
 /* make_plan (propagator.py:55-81).  kx2/ky2/kz2 are HOST arrays of the squared

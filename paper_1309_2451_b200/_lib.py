@@ -31,6 +31,7 @@ PASS_Y_FWD, PASS_Y_INV, PASS_Y_FWD_TO_PEER, PASS_Y_INV_FROM_PEER = range(5, 9)
 PASS_X_KIN, PASS_X_FWD, PASS_X_INV = range(9, 12)
 PASS_Y_FWD_BLK, PASS_X_KIN_BLK, PASS_Y_INV_BLK = range(12, 15)
 PASS_Y_FWD_TO_PEERS, PASS_X_KIN_TO_PEERS = 15, 16
+PASS_PZ_FIRST, PASS_PZ_MID, PASS_PZ_LAST, PASS_PY_FWD, PASS_PY_INV, PASS_PX_KIN = range(17, 23)
 
 # every symbol include/ctap.h declares
 EXPORTS = (
@@ -54,7 +55,7 @@ class CtapPlanDesc(ctypes.Structure):
         ("slab_r", ctypes.c_int32),
         ("phase_tables", ctypes.c_int32),
         ("dtype", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("pencil_c", ctypes.c_int32),
     ]
 
 

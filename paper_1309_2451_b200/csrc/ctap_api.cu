@@ -105,7 +105,16 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
     return fail(CTAP_EINVAL, "unknown mode %d", d->mode);
   if (d->dtype != CTAP_C128 && d->dtype != CTAP_C64) return fail(CTAP_EINVAL, "unknown dtype %d", d->dtype);
   int P = d->slab_p < 1 ? 1 : d->slab_p;
-  if (d->n[0] % P || d->n[1] % P) return fail(CTAP_EINVAL, "nx and ny must be divisible by the %d slab ranks", P);
+  const int Pc = d->pencil_c > 1 ? d->pencil_c : 0;
+  if (Pc) {
+    if (P % Pc) return fail(CTAP_EINVAL, "%d ranks do not form a pencil grid with %d columns", P, Pc);
+    const int Pr = P / Pc;
+    if (d->n[0] % Pr || d->n[1] % Pr || d->n[1] % Pc || d->n[2] % (8 * Pc))
+      return fail(CTAP_EINVAL, "pencil grid %d x %d needs nx %% %d, ny %% %d, ny %% %d and nz %% %d == 0", Pr, Pc, Pr,
+                  Pr, Pc, 8 * Pc);
+  } else if (d->n[0] % P || d->n[1] % P) {
+    return fail(CTAP_EINVAL, "nx and ny must be divisible by the %d slab ranks", P);
+  }
   if (d->slab_r < 0 || d->slab_r >= P) return fail(CTAP_EINVAL, "slab rank %d out of range", d->slab_r);
 
   ctap_plan* p = new ctap_plan();
@@ -114,6 +123,15 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   p->slab_p = P;
   p->slab_r = d->slab_r;
   p->nx_local = d->n[0] / P;
+  p->ny_pos = d->n[1];
+  if (Pc) {  // pencil: rank r = a Pc + b owns x block a, y block b
+    p->pen_c = Pc;
+    p->pen_r = P / Pc;
+    p->pen_a = d->slab_r / Pc;
+    p->pen_b = d->slab_r % Pc;
+    p->nx_local = d->n[0] / p->pen_r;
+    p->ny_pos = d->n[1] / Pc;
+  }
   p->mode = d->mode;
   p->dtype = d->dtype;
   p->e0 = d->e0;
@@ -173,7 +191,7 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   p->red_blocks = sms * 4;
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->red_partial, sizeof(double) * 8 * p->red_blocks);
-  const size_t nloc = (size_t)p->nx_local * d->n[1] * d->n[2];
+  const size_t nloc = (size_t)p->nx_local * p->ny_pos * d->n[2];
   const size_t csize = p->dtype == CTAP_C64 ? sizeof(float2) : sizeof(double2);
   // single GPU, opt-in (CTAP_KBLK_LX=lx > 0): out-of-place y passes into a
   // blocked k-space buffer so an x-line spans nx/2^lx address blocks instead of
@@ -191,11 +209,14 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
     if (e == cudaSuccess) e = cudaMalloc((void**)&p->vi_dev, sizeof(double) * nloc);
     if (e == cudaSuccess) e = ctap_run_v_internal(p, 0);
   }
-  if (e == cudaSuccess && v_dev && (d->phase_tables & 1) && d->mode == CTAP_REAL_TIME) {
+  // pencil plans compute both phases on the fly (the tables' layouts are the
+  // slab's; the phases are bitwise the same either way)
+  const int tables = Pc ? 0 : d->phase_tables;
+  if (e == cudaSuccess && v_dev && (tables & 1) && d->mode == CTAP_REAL_TIME) {
     e = cudaMalloc((void**)&p->expv_dev, csize * nloc);
     if (e == cudaSuccess) e = ctap_run_phase_table(p, 1, p->expv_dev, 0);
   }
-  if (e == cudaSuccess && (d->phase_tables & 2) && d->mode == CTAP_REAL_TIME) {
+  if (e == cudaSuccess && (tables & 2) && d->mode == CTAP_REAL_TIME) {
     e = cudaMalloc((void**)&p->expk_dev, csize * nloc);
     if (e == cudaSuccess) e = ctap_run_phase_table(p, 3, p->expk_dev, 0);
   }
@@ -233,17 +254,29 @@ CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, vo
   if (!p || !in || !out) return fail(CTAP_EINVAL, "null argument");
   const bool diag = kind == ctap::PASS_Y_COPY || kind == ctap::PASS_X_COPY || kind == ctap::PASS_XB_COPY ||
                     kind == ctap::PASS_XP_COPY || kind == ctap::PASS_XP_KIN || (kind >= ctap::PASS_WX_COPY && kind <= ctap::PASS_WY_FWD);
-  if (!diag && (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_X_KIN_TO_PEERS))
+  if (!diag && (kind < CTAP_PASS_Z_FWD || kind > CTAP_PASS_PX_KIN))
     return fail(CTAP_EINVAL, "unknown pass %d", kind);
   const bool blk = kind >= CTAP_PASS_Y_FWD_BLK && kind <= CTAP_PASS_Y_INV_BLK;
   if (blk && p->slab_p != 1) return fail(CTAP_EINVAL, "blocked k-space passes are single-GPU");
   if (blk && in == out && kind != CTAP_PASS_X_KIN_BLK) return fail(CTAP_EINVAL, "blocked y passes run out of place");
+  const bool pen = kind >= CTAP_PASS_PZ_FIRST && kind <= CTAP_PASS_PX_KIN;
+  if (pen != (p->pen_c > 0) && kind != CTAP_PASS_Z_FWD && kind != CTAP_PASS_Z_INV && !diag)
+    return fail(CTAP_EINVAL, pen ? "pencil pass %d on a plan without a pencil grid" : "slab pass %d on a pencil plan",
+                kind);
+  if ((kind == CTAP_PASS_PZ_FIRST || kind == CTAP_PASS_PZ_LAST || kind == CTAP_PASS_PY_FWD ||
+       kind == CTAP_PASS_PY_INV) && in == out)
+    return fail(CTAP_EINVAL, "pencil pass %d runs out of place", kind);
+  if ((kind == CTAP_PASS_PZ_MID || kind == CTAP_PASS_PX_KIN) && in != out)
+    return fail(CTAP_EINVAL, "pencil pass %d runs in place", kind);
+  if ((kind == CTAP_PASS_PZ_FIRST || kind == CTAP_PASS_PZ_MID || kind == CTAP_PASS_PZ_LAST) && !p->vi_dev)
+    return fail(CTAP_EINVAL, "pass %d needs a plan with a potential", kind);
   if (kind == CTAP_PASS_Y_FWD_TO_PEERS || kind == CTAP_PASS_X_KIN_TO_PEERS) {
     void* const* tab = kind == CTAP_PASS_Y_FWD_TO_PEERS ? p->peer_y : p->peer_p;
     for (int q = 0; q < p->slab_p; ++q)
       if (!tab[q]) return fail(CTAP_EINVAL, "peer buffers not registered (ctap_set_peer_buffers)");
   }
   if (kind <= CTAP_PASS_Z_LAST && in != out) return fail(CTAP_EINVAL, "z passes run in place");
+  if (p->pen_c && kind < CTAP_PASS_PZ_FIRST) return fail(CTAP_EINVAL, "pencil plans run the pencil passes only");
   if ((kind == CTAP_PASS_Z_FIRST || kind == CTAP_PASS_Z_MID || kind == CTAP_PASS_Z_LAST) && !p->vi_dev)
     return fail(CTAP_EINVAL, "plan has no potential");
   CUDA_TRY(ctap_run_pass(p, kind, in, out, (cudaStream_t)stream), "ctap_pass");
@@ -367,6 +400,7 @@ CTAP_API int ctap_density_xz(ctap_plan* p, const void* psi, double* out, void* s
 
 CTAP_API int ctap_k2_sums(ctap_plan* p, const void* phi, double* out, void* stream) {
   if (!p || !phi || !out) return fail(CTAP_EINVAL, "null argument");
+  if (p->pen_c) return fail(CTAP_EINVAL, "ctap_k2_sums takes slab (y-slab) layouts, not pencils");
   CUDA_TRY(ctap_run_k2_sums(p, phi, out, (cudaStream_t)stream), "ctap_k2_sums");
   return CTAP_OK;
 }
@@ -427,6 +461,7 @@ CTAP_API int ctap_phase_field(ctap_plan* p, int32_t which, void* out, void* stre
   if (!p || !out) return fail(CTAP_EINVAL, "null argument");
   if (which < 0 || which > 2) return fail(CTAP_EINVAL, "which must be 0 (v_half), 1 (v_full) or 2 (k)");
   if (which < 2 && !p->vi_dev) return fail(CTAP_EINVAL, "plan has no potential");
+  if (p->pen_c) return fail(CTAP_EINVAL, "ctap_phase_field takes slab plans");
   CUDA_TRY(ctap_run_phase_field(p, which, out, (cudaStream_t)stream), "ctap_phase_field");
   return CTAP_OK;
 }

@@ -29,6 +29,12 @@ enum PassKind {
   PASS_Y_INV_BLK = CTAP_PASS_Y_INV_BLK,  // y^-1, blocked buffer -> natural
   PASS_Y_FWD_TO_PEERS = CTAP_PASS_Y_FWD_TO_PEERS,
   PASS_X_KIN_TO_PEERS = CTAP_PASS_X_KIN_TO_PEERS,
+  PASS_PZ_FIRST = CTAP_PASS_PZ_FIRST,
+  PASS_PZ_MID = CTAP_PASS_PZ_MID,
+  PASS_PZ_LAST = CTAP_PASS_PZ_LAST,
+  PASS_PY_FWD = CTAP_PASS_PY_FWD,
+  PASS_PY_INV = CTAP_PASS_PY_INV,
+  PASS_PX_KIN = CTAP_PASS_PX_KIN,
   // diagnostics: the strided passes' memory traffic without the transforms
   PASS_Y_COPY = 60,
   PASS_X_COPY = 61,
@@ -47,8 +53,10 @@ enum PassKind {
 
 struct ctap_plan {
   int64_t n[3];
-  int64_t nx_local;
+  int64_t nx_local;        // x extent of this rank's position-space block
+  int64_t ny_pos;          // y extent of it (ny for slabs, ny/Pc for pencils)
   int slab_p, slab_r;
+  int pen_c, pen_r, pen_a, pen_b;  // pencil grid Pr x Pc and this rank's (a, b); pen_c = 0 for slabs
   int mode;  // 0 real, 1 imaginary
   double e0, dt_i, len2, v_shift;
   double inv_scale;        // 1 / (nx ny nz), exact power of two

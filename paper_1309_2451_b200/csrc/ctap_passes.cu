@@ -72,6 +72,10 @@ struct ZArgs {
   void* psi;
   uint32_t nlines;  // nx_local * ny
   PhaseArgs ph;
+  // pencil z-chunked side (CH bit 0: input, bit 1: output): point z of line l
+  // at (z >> lzc) cs + l 2^lzc + (z & (2^lzc - 1)), cs = nlines 2^lzc
+  void* out;
+  uint32_t lzc, cs;
 };
 
 template <int L, int KIND, bool VTAB, typename CV, typename Sync>
@@ -117,21 +121,26 @@ struct ZMinBlocks {
   static constexpr int value = (KIND == T_VMID && VTAB) ? CTAP_Z_MINB_TAB : CTAP_Z_MINB;
 };
 
-template <int L, int KIND, bool VTAB, typename CV>
+template <int L, int KIND, bool VTAB, typename CV, int CH = 0>
 __global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::value) zline_kernel(ZArgs a, const TwOf<CV>* __restrict__ tw) {
   using Cfg = ZCfg<L, CV>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CV* smem = reinterpret_cast<CV*>(smem_raw);
-  CV* psi = (CV*)a.psi;
+  const CV* in = (const CV*)a.psi;
+  CV* psi = (CV*)a.out;  // == a.psi for the in-place natural and z-chunked passes
   const int t = threadIdx.x % Cfg::T;
   const int c = threadIdx.x / Cfg::T;
   const uint32_t line = blockIdx.x * Cfg::C + c;
   const bool active = line < a.nlines;
   const uint32_t off = line * L;
+  // element z of this line: natural off + z, or z-chunked (pencil)
+  const uint32_t zmask = (1u << a.lzc) - 1u, coff = line << a.lzc;
+  auto at_in = [&](uint32_t zz) { return CH & 1 ? (zz >> a.lzc) * a.cs + coff + (zz & zmask) : off + zz; };
+  auto at_out = [&](uint32_t zz) { return CH & 2 ? (zz >> a.lzc) * a.cs + coff + (zz & zmask) : off + zz; };
   SmemContig<CV> sm{smem + c * Cfg::smem_line};
   CV v[kElems];
 #pragma unroll
-  for (int m = 0; m < kElems; ++m) v[m] = active ? __ldcg(&psi[off + t + m * Cfg::T]) : CT<CV>::mk(0, 0);
+  for (int m = 0; m < kElems; ++m) v[m] = active ? __ldcg(&in[at_in(t + m * Cfg::T)]) : CT<CV>::mk(0, 0);
   if constexpr (Cfg::T <= 32) {
     z_body<L, KIND, VTAB>(a, v, t, off, active, tw, sm, SyncWarp{});
   } else {
@@ -139,7 +148,7 @@ __global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::
   }
   if (active) {
 #pragma unroll
-    for (int m = 0; m < kElems; ++m) __stcg(&psi[off + t + m * Cfg::T], v[m]);
+    for (int m = 0; m < kElems; ++m) __stcg(&psi[at_out(t + m * Cfg::T)], v[m]);
   }
 }
 
@@ -218,10 +227,10 @@ static cudaError_t allow_smem(K k, size_t bytes) {
                            : cudaSuccess;
 }
 
-template <int L, int KIND, bool VTAB, typename CV>
+template <int L, int KIND, bool VTAB, typename CV, int CH = 0>
 static cudaError_t launch_z(const ZArgs& a, const TwOf<CV>* tw, cudaStream_t st) {
   using Cfg = ZCfg<L, CV>;
-  auto k = zline_kernel<L, KIND, VTAB, CV>;
+  auto k = zline_kernel<L, KIND, VTAB, CV, CH>;
   static cudaError_t init = allow_smem(k, Cfg::smem);
   if (init != cudaSuccess) return init;
   k<<<(a.nlines + Cfg::C - 1) / Cfg::C, Cfg::threads, Cfg::smem, st>>>(a, tw);
@@ -258,9 +267,10 @@ struct Tw {
   const float4* f;
 };
 
-template <int KIND, bool VTAB>
+template <int KIND, bool VTAB, int CH = 0>
 static cudaError_t dispatch_z(int L, bool c64, const ZArgs& a, Tw tw, cudaStream_t st) {
-#define CTAP_Z(LL) (c64 ? launch_z<LL, KIND, VTAB, float2>(a, tw.f, st) : launch_z<LL, KIND, VTAB, double2>(a, tw.d, st))
+#define CTAP_Z(LL) \
+  (c64 ? launch_z<LL, KIND, VTAB, float2, CH>(a, tw.f, st) : launch_z<LL, KIND, VTAB, double2, CH>(a, tw.d, st))
   CTAP_BY_LENGTH(L, CTAP_Z)
 #undef CTAP_Z
 }
@@ -353,7 +363,7 @@ std::vector<double> ctap_make_twiddles(int off[8]) {
 }
 
 cudaError_t ctap_run_v_internal(const ctap_plan* p, cudaStream_t st) {
-  const uint32_t n = (uint32_t)(p->nx_local * p->n[1] * p->n[2]);
+  const uint32_t n = (uint32_t)(p->nx_local * p->ny_pos * p->n[2]);
   v_internal_kernel<<<p->red_blocks, 256, 0, st>>>(p->v_dev, p->vi_dev, n, p->v_shift, p->e0);
   return cudaGetLastError();
 }
@@ -453,10 +463,62 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
     ph.kval[i] = p->kval[i];
   }
 
+  if (kind >= PASS_PZ_FIRST && kind <= PASS_PX_KIN) {  // pencil decomposition (include/ctap.h)
+    if (!p->pen_c || zsub) return cudaErrorInvalidValue;
+    const uint32_t Pr = (uint32_t)p->pen_r, Pc = (uint32_t)p->pen_c;
+    const uint32_t xa = (uint32_t)p->nx_local, yb = (uint32_t)(ny / Pc), yd = (uint32_t)(ny / Pr);
+    const uint32_t zc = (uint32_t)(nz / Pc);
+    if (kind <= PASS_PZ_LAST) {
+      ZArgs a;
+      a.psi = const_cast<void*>(in);
+      a.out = out;
+      a.nlines = xa * yb;
+      a.ph = ph;
+      a.lzc = (uint32_t)ilog2(zc);
+      a.cs = a.nlines * zc;
+      const Tw tw = twid(p, nz);
+      if (kind == PASS_PZ_FIRST) return dispatch_z<T_VFIRST, false, 2>((int)nz, c64, a, tw, st);
+      if (kind == PASS_PZ_MID) return dispatch_z<T_VMID, false, 3>((int)nz, c64, a, tw, st);
+      return dispatch_z<T_VLAST, false, 1>((int)nz, c64, a, tw, st);
+    }
+    constexpr int kNone = 31;
+    TileArgs a;
+    a.in = in;
+    a.out = out;
+    a.nchunk = zc / 8;
+    a.ph = ph;
+    if (kind == PASS_PX_KIN) {  // natural (nx, ny/Pr, nz/Pc): ky offset a ny/Pr, kz offset b nz/Pc
+      a.n_outer = yd;
+      a.lin = a.lout = Layout{zc, 0u, yd * zc, 0, 0u, kNone};
+      a.ph.outer_off = (uint32_t)p->pen_a * yd;
+      a.ph.z_off = (uint32_t)p->pen_b * zc;
+      if (in == out) {
+        cudaError_t e = ctap_run_wline(p, 2, T_KIN, p->wline, out, a, st);
+        if (e != cudaErrorNotSupported) return e;
+      }
+      return dispatch_tile<T_KIN, false, false, false>((int)nx, c64, a, twid(p, nx), st);
+    }
+    // y passes between the row-exchange layout Yb = [b'][x][y % yb][z'] and
+    // the column-exchange layout Xp = [a'][x][y % yd][z'] (blocked by y)
+    a.n_outer = xa;
+    const Layout yblk{yb * zc, xa * yb * zc, zc, ilog2(yb), 0u, kNone};
+    const Layout xblk{yd * zc, xa * yd * zc, zc, ilog2(yd), 0u, kNone};
+    if (kind == PASS_PY_FWD) {
+      a.lin = yblk;
+      a.lout = xblk;
+      return dispatch_tile<T_FWD, true, true, false>((int)ny, c64, a, twid(p, ny), st);
+    }
+    a.lin = xblk;
+    a.lout = yblk;
+    return dispatch_tile<T_INV, true, true, false>((int)ny, c64, a, twid(p, ny), st);
+  }
   if (kind >= PASS_Z_FWD && kind <= PASS_Z_LAST) {
     if (in != out) return cudaErrorInvalidValue;
     ZArgs a;
     a.psi = out;
+    a.out = out;
+    a.lzc = 0;
+    a.cs = 0;
     a.nlines = (uint32_t)(p->nx_local * ny);
     a.ph = ph;
     const Tw tw = twid(p, nz);

@@ -63,7 +63,7 @@ struct ObserveF {
   const double* xs;
   const double* xb1;
   const double* xb2;
-  int64_t nyz, ny, nz, nx_global, x_off;
+  int64_t nyz, ny, nz, nx_global, x_off, ny_global, y_off;
   int margin;
   __device__ __forceinline__ void operator()(int64_t i, double (&acc)[5]) const {
     const CV a = psi[i];
@@ -82,8 +82,9 @@ struct ObserveF {
       if (!(in_l || in_r)) acc[2] += rho;
     }
     int64_t gx = x + x_off;
-    bool edge = gx < margin || gx >= nx_global - margin || y < margin || y >= ny - margin || z < margin ||
-                z >= nz - margin;
+    int64_t gy = y + y_off;
+    bool edge = gx < margin || gx >= nx_global - margin || gy < margin || gy >= ny_global - margin ||
+                z < margin || z >= nz - margin;
     if (edge) acc[4] += rho;
   }
 };
@@ -172,11 +173,14 @@ static cudaError_t observe_t(const ctap_plan* p, const void* psi, const double* 
   f.xs = xs;
   f.xb1 = xb1;
   f.xb2 = xb2;
-  f.nyz = p->n[1] * p->n[2];
-  f.ny = p->n[1];
+  f.nyz = p->ny_pos * p->n[2];
+  f.ny = p->ny_pos;
   f.nz = p->n[2];
   f.nx_global = p->n[0];
-  f.x_off = (int64_t)p->slab_r * p->nx_local;
+  f.ny_global = p->n[1];
+  // slab: x block slab_r; pencil: x block a, y block b
+  f.x_off = (int64_t)(p->pen_c ? p->pen_a : p->slab_r) * p->nx_local;
+  f.y_off = p->pen_c ? (int64_t)p->pen_b * p->ny_pos : 0;
   f.margin = margin;
   return run_reduce<5>(p, f, p->nx_local * f.nyz, out, st);
 }
@@ -210,7 +214,7 @@ static cudaError_t v_t(const ctap_plan* p, const void* psi, double* out, cudaStr
   VF<CV> f;
   f.psi = (const CV*)psi;
   f.V = p->v_dev;
-  return run_reduce<2>(p, f, p->nx_local * p->n[1] * p->n[2], out, st);
+  return run_reduce<2>(p, f, p->nx_local * p->ny_pos * p->n[2], out, st);
 }
 
 cudaError_t ctap_run_v_sums(const ctap_plan* p, const void* psi, double* out, cudaStream_t st) {
@@ -222,14 +226,14 @@ cudaError_t ctap_run_density_xz(const ctap_plan* p, const void* psi, double* out
   int threads = 256;
   const unsigned blocks = (unsigned)((n + threads - 1) / threads);
   if (p->dtype == CTAP_C64)
-    density_xz_kernel<<<blocks, threads, 0, st>>>((const float2*)psi, p->nx_local, p->n[1], p->n[2], out);
+    density_xz_kernel<<<blocks, threads, 0, st>>>((const float2*)psi, p->nx_local, p->ny_pos, p->n[2], out);
   else
-    density_xz_kernel<<<blocks, threads, 0, st>>>((const double2*)psi, p->nx_local, p->n[1], p->n[2], out);
+    density_xz_kernel<<<blocks, threads, 0, st>>>((const double2*)psi, p->nx_local, p->ny_pos, p->n[2], out);
   return cudaGetLastError();
 }
 
 cudaError_t ctap_run_scale(const ctap_plan* p, void* psi, double d, cudaStream_t st) {
-  int64_t n = p->nx_local * p->n[1] * p->n[2];
+  int64_t n = p->nx_local * p->ny_pos * p->n[2];
   if (p->dtype == CTAP_C64)
     scale_kernel<<<p->red_blocks, kRedThreads, 0, st>>>((float2*)psi, n, d);
   else

@@ -57,7 +57,7 @@ class NativePlan:
 
     def __init__(self, grid, v_dev: torch.Tensor | None, mass: float, dt: float,
                  mode: str = REAL_TIME, v_shift: float = 0.0, slab_p: int = 1, slab_r: int = 0,
-                 phase_tables: int = 0, precision: str = "complex128"):
+                 phase_tables: int = 0, precision: str = "complex128", pencil_c: int = 0):
         lib = _lib.load()
         dev = _device.require_cuda()
         self.grid = as_simgrid(grid)
@@ -73,6 +73,7 @@ class NativePlan:
         desc.slab_p = int(slab_p)
         desc.slab_r = int(slab_r)
         desc.phase_tables = int(phase_tables)
+        desc.pencil_c = int(pencil_c)
         if precision not in PRECISIONS:
             raise ValueError(f"unknown precision {precision!r}; known: {sorted(PRECISIONS)}")
         desc.dtype = _lib.DTYPE_C64 if precision == "complex64" else _lib.DTYPE_C128
