@@ -166,6 +166,58 @@ __device__ __forceinline__ void column(const SwzCol& col, int lane, const double
   for (int m = 0; m < E; ++m) col.nat(lane + 32 * m) = v[m];
 }
 
+// The same transform with TWO warps per column (64 threads, E = L/64 points
+// each, named barrier per column): the ring then computes one tile with all
+// 16 warps while two tiles load.  The kx-mirror factors cross the two warps,
+// so they are exchanged through the column's own slots (indices < L/2,
+// free between the transforms).
+template <int L, int KIND>
+__device__ __forceinline__ void column2(const SwzCol& col, int ct, const double2* __restrict__ tw,
+                                        const PhaseArgs& ph, uint32_t o, uint32_t z, SyncNamed sync) {
+  constexpr int E = L / 64;
+  static_assert(E >= 8, "two warps per column need L >= 512 (radix-8 stages)");
+  double2 v[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) v[m] = col.nat(ct + 64 * m);
+  sync();
+  if constexpr (KIND == T_COPY) {
+  } else if constexpr (KIND == T_FWD) {
+    line_fft<L, -1, E>(v, ct, tw, col, sync);
+  } else if constexpr (KIND == T_INV) {
+    line_fft<L, +1, E>(v, ct, tw, col, sync);
+  } else {  // T_KIN
+    double ky2, kz2;
+    if (ph.kgen) {
+      ky2 = k2_gen(ph.outer_off + o, ph.kn[1], ph.kval[1]);
+      kz2 = k2_gen(ph.z_off + z, ph.kn[2], ph.kval[2]);
+    } else {
+      ky2 = __ldg(&ph.ky2[ph.outer_off + o]);
+      kz2 = __ldg(&ph.kz2[ph.z_off + z]);
+    }
+    line_fft<L, -1, E>(v, ct, tw, col, sync);
+    // factors of this thread's points below L/2, published in their slots
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+      const double2 f = kfactor(kx2_of(ct + 64 * m, ph), ky2, kz2, ph);
+      col.nat(ct + 64 * m) = f;
+      apply_k(v[m], f, ph.imag);
+    }
+    // index L/2 (thread 0's self-mirrored point m = E/2): warp 0 only
+    double2 fn = make_double2(0.0, 0.0);
+    if (ct < 32) fn = kfactor(kx2_of(L / 2, ph), ky2, kz2, ph);
+    sync();
+#pragma unroll
+    for (int m = E / 2; m < E; ++m) {
+      const int idx = L - (ct + 64 * m);  // the mirror point, < L/2 except ct = 0, m = E/2
+      apply_k(v[m], idx == L / 2 ? fn : col.nat(idx), ph.imag);
+    }
+    sync();
+    line_fft<L, +1, E>(v, ct, tw, col, sync);
+  }
+#pragma unroll
+  for (int m = 0; m < E; ++m) col.nat(ct + 64 * m) = v[m];
+}
+
 // ---------------------------------------------------------------------------
 // mover 1: persistent TMA ring
 // ---------------------------------------------------------------------------
@@ -181,7 +233,7 @@ struct NoPeers {};
 // AXIS 1 / 2: y / x lines of the natural layout (in place); AXIS 4: x lines of
 // the slab's y-slab, results stored by TMA straight into the other ranks'
 // buffers (the transpose of the fused slab transport).
-template <int L, int KIND, int AXIS, typename PM>
+template <int L, int KIND, int AXIS, typename PM, int WPC = 1>
 __global__ void __launch_bounds__(kRingThreads, 1)
     ring_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a, const double2* __restrict__ tw,
                 const __grid_constant__ PM pm) {
@@ -214,10 +266,12 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       tma_load(buf + q * BOX * kCols, &tmap, &full[b], c0, AXIS != 1 ? o : q * BOX, AXIS != 1 ? q * BOX : o);
   };
 
+  constexpr int kWarpsPerTile = kCols * WPC;           // WPC 2: all 16 warps on one tile
+  constexpr int kTileGroups = kGroups * kCols / kWarpsPerTile;
   if (threadIdx.x == 0) {
     for (int b = 0; b < kBufs; ++b) {
       bar_init(&full[b], 1);
-      bar_init(&done[b], kCols);
+      bar_init(&done[b], kWarpsPerTile);
       cnt[b] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -225,8 +279,8 @@ __global__ void __launch_bounds__(kRingThreads, 1)
   }
   __syncthreads();
 
-  const int g = warp / kCols, c = warp % kCols;
-  for (uint32_t j = g; j < nloc; j += kGroups) {
+  const int g = warp / kWarpsPerTile, c = (warp % kWarpsPerTile) / WPC;
+  for (uint32_t j = g; j < nloc; j += kTileGroups) {
     const int b = j % kBufs;
     const uint32_t k = j / kBufs;
     // fill k - 1 of this buffer (the other group's tile) must be consumed
@@ -237,7 +291,11 @@ __global__ void __launch_bounds__(kRingThreads, 1)
     const uint32_t o = tile / a.nchunk;
     const uint32_t z = (tile - o * a.nchunk) * 8 + c;
     double2* buf = bufs + (size_t)b * L * kCols;
-    column<L, KIND>(SwzCol{buf, c}, lane, tw, a.ph, o, z);
+    if constexpr (WPC == 1) {
+      column<L, KIND>(SwzCol{buf, c}, lane, tw, a.ph, o, z);
+    } else {
+      column2<L, KIND>(SwzCol{buf, c}, (warp & 1) * 32 + lane, tw, a.ph, o, z, SyncNamed{1 + c, 64});
+    }
     fence_async_smem();  // generic-proxy writes -> the TMA store
     __syncwarp();
     if (lane == 0) {
@@ -245,7 +303,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       // with tile j + kBufs (a dedicated producer warp would make 17 warps and
       // cap the registers at 96 per thread)
       __threadfence_block();
-      const bool last = atomicAdd(&cnt[b], 1u) == kCols - 1;
+      const bool last = atomicAdd(&cnt[b], 1u) == kWarpsPerTile - 1;
       __threadfence_block();
       bar_arrive(&done[b]);
       if (last) {
@@ -341,7 +399,7 @@ static int sm_count() {
 // AXIS 2: x lines of an (L, n_outer, nz) array; AXIS 1: y lines of an
 // (n_outer, L, nz) array (nz = 8 * a.nchunk)
 template <int L, int KIND, int AXIS>
-static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw, cudaStream_t st) {
+static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw, cudaStream_t st, int wpc = 1) {
   constexpr int BOX = L < 256 ? L : 256;
   EncodeTiledFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
@@ -357,11 +415,15 @@ static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  auto k = ring_kernel<L, KIND, AXIS, NoPeers>;
+  auto k = ring_kernel<L, KIND, AXIS, NoPeers, 1>;
+  if constexpr (L >= 512 && KIND == T_KIN)
+    if (wpc == 2) k = ring_kernel<L, KIND, AXIS, NoPeers, 2>;
   constexpr size_t smem =
       (size_t)kBufs * L * kCols * sizeof(double2) + 2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t) + 1024;
-  static cudaError_t init = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (init != cudaSuccess) return init;
+  static cudaError_t init[2] = {cudaErrorNotReady, cudaErrorNotReady};
+  cudaError_t& ini = init[wpc == 2 ? 1 : 0];
+  if (ini == cudaErrorNotReady) ini = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (ini != cudaSuccess) return ini;
   const uint32_t ntiles = a.n_outer * a.nchunk;
   const uint32_t grid = ntiles < (uint32_t)sm_count() ? ntiles : (uint32_t)sm_count();
   k<<<grid, kRingThreads, smem, st>>>(map, a, tw, NoPeers{});
@@ -435,17 +497,19 @@ using namespace ctap;
 // In-place strided pass on lines of length L = 256 or 512 through the
 // warp-per-line kernels: axis 2 = x lines of an (L, n_outer, nz) array
 // (kinds T_FWD, T_INV, T_KIN, T_COPY), axis 1 = y lines of an (n_outer, L, nz)
-// array (T_FWD, T_INV, T_COPY).  `mode` 1 ring, 2 tile; returns
+// array (T_FWD, T_INV, T_COPY).  `mode` 1 ring, 2 tile, 3 ring with two warps
+// per column for the 512-point kinetic pass (else as 1); returns
 // cudaErrorNotSupported outside these shapes (the caller then uses tile_kernel).
 cudaError_t ctap_run_wline(const ctap_plan* p, int axis, int kind, int mode, void* data, const TileArgs& a,
                            cudaStream_t st) {
-  if (p->dtype != CTAP_C128 || mode < 1 || mode > 2) return cudaErrorNotSupported;
+  if (p->dtype != CTAP_C128 || mode < 1 || mode > 3) return cudaErrorNotSupported;
   const int64_t L = axis == 2 ? p->n[0] : p->n[1];
   if (L != 256 && L != 512) return cudaErrorNotSupported;
   if (axis == 1 && kind == T_KIN) return cudaErrorNotSupported;
   const double2* tw = p->twiddles + p->tw_off[L == 256 ? 5 : 6];
-#define CTAP_WL_K(LL, KK, AX) \
-  (mode == 1 ? wl::launch_ring<LL, KK, AX>(a, data, tw, st) : wl::launch_tile1<LL, KK, AX>(a, data, tw, st))
+#define CTAP_WL_K(LL, KK, AX)                                                                       \
+  (mode != 2 ? wl::launch_ring<LL, KK, AX>(a, data, tw, st, mode == 3 ? 2 : 1)                      \
+             : wl::launch_tile1<LL, KK, AX>(a, data, tw, st))
 #define CTAP_WL(LL, AX)                          \
   switch (kind) {                                \
     case T_FWD: return CTAP_WL_K(LL, T_FWD, AX); \

@@ -280,7 +280,8 @@ def test_complex64_has_no_systematic_rounding_drift():
 def test_wline_bitwise_equals_tile_kernel(monkeypatch, n):
     """The warp-per-line x-pass kernels (CTAP_WLINE=1 TMA ring, 2 one tile per
     CTA) use the same radix plan, twiddles and exact kinetic phase as
-    tile_kernel (CTAP_WLINE=0): 30 steps must agree bit for bit, in real and
+    tile_kernel (CTAP_WLINE=0), also with two warps per column (3): 30 steps
+    must agree bit for bit, in real and
     imaginary time."""
     grid = qgrid.make_grid(*n, (20e-6, 4e-6, 250e-6), origin=(-10e-6, 4e-6 / n[1] / 2, 0.0))
     rng = np.random.default_rng(7)
@@ -302,3 +303,4 @@ def test_wline_bitwise_equals_tile_kernel(monkeypatch, n):
         ref = run("0", kind)
         assert np.array_equal(run("1", kind), ref)
         assert np.array_equal(run("2", kind), ref)
+        assert np.array_equal(run("3", kind), ref)
