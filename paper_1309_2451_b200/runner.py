@@ -200,3 +200,72 @@ def run_sweep(cfg, out_dir=None, group=None, run_point=None) -> list:
             for i_m, ordering, pr in rows:
                 fh.write(f"{i_m:.17g},{ordering},{pr:.17g}\n")
     return rows
+
+
+# ---------------------------------------------------------------------------
+# the measurement harness (runner.py:260-325)
+# ---------------------------------------------------------------------------
+
+def bench_thread_counts(max_threads: int | None = None) -> list:
+    """Powers of two up to the host thread count, plus the count itself
+    (runner.py:260-268).  The device path ignores the count (make_plan's
+    `threads` is accepted for signature compatibility), so every row of a
+    run_bench report times the same B200 kernels."""
+    hw = max_threads or (os.cpu_count() or 1)
+    counts, c = [], 1
+    while c < hw:
+        counts.append(c)
+        c *= 2
+    counts.append(hw)
+    return sorted(set(counts))
+
+
+def run_bench(cfg, out_dir, thread_counts=None, warm_steps: int | None = None,
+              timed_steps: int | None = None, chunks: int = 10) -> dict:
+    """Split-step steps/sec on the configured grid (runner.py:271-325) on the
+    device: the reference's synthetic harmonic trap and Gaussian packet, warm
+    steps discarded, the timed steps in `chunks` evolve_real calls, median
+    chunk rate (spread min..max), written to bench.csv / bench.txt in the
+    reference's format.  One row per entry of `thread_counts` (default
+    [1]: the device does not depend on the host thread count)."""
+    from .qgrid import gaussian_packet
+
+    os.makedirs(out_dir, exist_ok=True)
+    warm = cfg.bench_warm_steps if warm_steps is None else warm_steps
+    timed = cfg.bench_timed_steps if timed_steps is None else timed_steps
+    grid = cfg.to_grid()
+    x, y, z = grid.meshgrid()
+    center = [o + e / 2 for o, e in zip(grid.origin, grid.extents)]
+    v = 0.5 * cfg.mass * cfg.omega_z ** 2 * ((x - center[0]) ** 2 + (y - center[1]) ** 2
+                                             + (z - center[2]) ** 2)
+    psi0 = gaussian_packet(grid, center, [e / 16 for e in grid.extents])
+    report = {"grid": grid.n, "warm_steps": warm, "timed_steps": timed, "rates": {}}
+    for nt in (thread_counts or [1]):
+        plan = make_plan(grid, v, cfg.mass, cfg.dt, mode=REAL_TIME, threads=nt)
+        psi = psi0.copy()
+        evolve_real(psi, plan, warm)
+        per_chunk = max(1, timed // chunks)
+        rates = []
+        for _ in range(chunks):
+            psi, stats = evolve_real(psi, plan, per_chunk)
+            rates.append(stats.steps_per_second)
+        rates = np.array(rates)
+        report["rates"][nt] = {"median": float(np.median(rates)), "min": float(rates.min()),
+                               "max": float(rates.max())}
+    csv_path = os.path.join(out_dir, "bench.csv")
+    with open(csv_path, "w") as fh:
+        fh.write("threads,steps_per_sec\n")
+        for nt, r in report["rates"].items():
+            fh.write(f"{nt},{r['median']:.17g}\n")
+    ref_steps = 100_000  # reference-chip full run at dt = 1 us
+    txt_path = os.path.join(out_dir, "bench.txt")
+    with open(txt_path, "w") as fh:
+        fh.write(f"split-operator kernel benchmark, grid {grid.n} (B200, libctap)\n")
+        fh.write(f"warm {warm} steps discarded, {timed} timed steps in {chunks} chunks\n")
+        for nt, r in report["rates"].items():
+            fh.write(f"threads={nt}: median {r['median']:.3f} steps/s "
+                     f"(spread {r['min']:.3f}..{r['max']:.3f}); projected "
+                     f"{ref_steps}-step run: {ref_steps / r['median'] / 3600:.4f} h\n")
+    report["csv"] = csv_path
+    report["txt"] = txt_path
+    return report

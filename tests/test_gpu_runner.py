@@ -110,3 +110,35 @@ def test_run_sweep_single_replica(tmp_path):
     direct = runner.evolve_point(cfg, i_middle=float(cfg.sweep_values()[1]))["final_p_r"]
     assert rows[1][2] == direct
     assert (tmp_path / "sweep.csv").exists()
+
+
+@dataclasses.dataclass(frozen=True)
+class BenchConfig:
+    """The fields of ExperimentConfig that run_bench reads (defaults of the
+    reference config: 64^3 over 20 x 4 x 1000 um, f_z = 5 Hz, dt = 1 us)."""
+
+    mass: float
+    omega_z: float = 2 * np.pi * 5.0
+    dt: float = 1e-6
+    bench_warm_steps: int = 100
+    bench_timed_steps: int = 300
+
+    def to_grid(self):
+        return qgrid.make_grid(64, 64, 64, (20e-6, 4e-6, 1000e-6), origin=(-10e-6, 4e-6 / 128, 0.0))
+
+
+def test_run_bench_reports_and_files(tmp_path):
+    """runner.run_bench (runner.py:271-325): median/min/max chunk rates per
+    thread count, bench.csv and bench.txt in the reference's format."""
+    from paper_1309_2451_b200.constants import species_mass
+
+    cfg = BenchConfig(mass=species_mass("li6"))
+    rep = runner.run_bench(cfg, str(tmp_path), thread_counts=[1, 2], warm_steps=20, timed_steps=100, chunks=5)
+    assert rep["grid"] == (64, 64, 64) and set(rep["rates"]) == {1, 2}
+    for r in rep["rates"].values():
+        assert 0 < r["min"] <= r["median"] <= r["max"]
+    lines = open(rep["csv"]).read().splitlines()
+    assert lines[0] == "threads,steps_per_sec" and len(lines) == 3
+    assert float(lines[1].split(",")[1]) == rep["rates"][1]["median"]
+    txt = open(rep["txt"]).read()
+    assert "warm 20 steps discarded, 100 timed steps in 5 chunks" in txt and "threads=2: median" in txt

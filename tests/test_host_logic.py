@@ -147,3 +147,14 @@ def test_unknown_precision_rejected():
     g = qgrid.make_grid(8, 8, 8, (1e-5,) * 3)
     with pytest.raises((ValueError, RuntimeError)):
         prop.make_plan(g, np.zeros(g.n), M, 1e-6, precision="complex32")
+
+
+def test_bench_thread_counts_matches_reference_rule():
+    """runner.bench_thread_counts (runner.py:260-268): powers of two below the
+    host thread count, plus the count."""
+    from paper_1309_2451_b200.runner import bench_thread_counts
+
+    assert bench_thread_counts(1) == [1]
+    assert bench_thread_counts(6) == [1, 2, 4, 6]
+    assert bench_thread_counts(8) == [1, 2, 4, 8]
+    assert bench_thread_counts(16) == [1, 2, 4, 8, 16]
