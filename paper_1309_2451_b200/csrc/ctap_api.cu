@@ -152,9 +152,9 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   p->kgen = 1;
   for (int i = 0; i < 3; ++i) p->kgen &= recover_kval(k2h[i], d->n[i], &p->kval[i]);
   if (const char* env = getenv("CTAP_KGEN")) p->kgen &= atoi(env) != 0;
-  // x-pass kernel of the single-GPU step: 1 warp-per-line TMA ring (default),
-  // 2 warp-per-line one tile per CTA, 3 ring with two warps per column
-  // (nx = 512), 0 tile_kernel (ctap_wline.cu)
+  // x-pass kernel of the single-GPU step: 1 warp-per-line TMA ring (default;
+  // nx = 512), 2 warp-per-line one tile per CTA, 3 ring with two warps per
+  // column, 4-6 the same also for nx = 256, 0 tile_kernel (ctap_wline.cu)
   p->wline = 1;
   if (const char* env = getenv("CTAP_WLINE")) p->wline = atoi(env);
   p->zchunk = 0;

@@ -502,9 +502,14 @@ using namespace ctap;
 // cudaErrorNotSupported outside these shapes (the caller then uses tile_kernel).
 cudaError_t ctap_run_wline(const ctap_plan* p, int axis, int kind, int mode, void* data, const TileArgs& a,
                            cudaStream_t st) {
-  if (p->dtype != CTAP_C128 || mode < 1 || mode > 3) return cudaErrorNotSupported;
+  if (p->dtype != CTAP_C128 || mode < 1 || mode > 6) return cudaErrorNotSupported;
   const int64_t L = axis == 2 ? p->n[0] : p->n[1];
   if (L != 256 && L != 512) return cudaErrorNotSupported;
+  // the 256-point kinetic pass stays on tile_kernel: with 8 points per lane
+  // the ring measured slower there (0.158 vs 0.144 ms at 256^3); the
+  // CTAP_WLINE >= 4 switch forces it (tests)
+  if (axis == 2 && kind == T_KIN && L == 256 && mode < 4) return cudaErrorNotSupported;
+  if (mode >= 4) mode -= 3;
   if (axis == 1 && kind == T_KIN) return cudaErrorNotSupported;
   const double2* tw = p->twiddles + p->tw_off[L == 256 ? 5 : 6];
 #define CTAP_WL_K(LL, KK, AX)                                                                       \
@@ -532,10 +537,10 @@ cudaError_t ctap_run_wline(const ctap_plan* p, int axis, int kind, int mode, voi
 // with per-rank TMA stores; cudaErrorNotSupported outside complex128,
 // nx = 256 / 512 (the caller then uses tile_kernel's peer stores).
 cudaError_t ctap_run_wline_peers(const ctap_plan* p, const void* in, const TileArgs& a, cudaStream_t st) {
-  if (p->dtype != CTAP_C128 || p->wline != 1) return cudaErrorNotSupported;
+  if (p->dtype != CTAP_C128 || (p->wline != 1 && p->wline != 4)) return cudaErrorNotSupported;
   const int64_t L = p->n[0];
   const double2* tw = p->twiddles + p->tw_off[L == 256 ? 5 : 6];
   if (L == 512) return wl::launch_ring_peers<512>(a, in, p->slab_p, tw, st);
-  if (L == 256) return wl::launch_ring_peers<256>(a, in, p->slab_p, tw, st);
+  if (L == 256 && p->wline >= 4) return wl::launch_ring_peers<256>(a, in, p->slab_p, tw, st);
   return cudaErrorNotSupported;
 }

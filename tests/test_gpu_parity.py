@@ -299,8 +299,8 @@ def test_wline_bitwise_equals_tile_kernel(monkeypatch, n):
                 psi = propagator.step(psi, plan)
         return psi.amplitudes
 
+    modes = ("1", "2", "3") if n[0] == 512 else ("4", "5", "6")  # 4-6: the ring also at nx = 256
     for kind in ("real_time", "imaginary_time"):
         ref = run("0", kind)
-        assert np.array_equal(run("1", kind), ref)
-        assert np.array_equal(run("2", kind), ref)
-        assert np.array_equal(run("3", kind), ref)
+        for mode in modes:
+            assert np.array_equal(run(mode, kind), ref)

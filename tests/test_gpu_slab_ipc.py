@@ -71,9 +71,9 @@ def _worker(rank, world, port, steps, out, n):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, (32, 16, 32)), (2, (256, 16, 16))])
+@pytest.mark.parametrize("world,n", [(2, (32, 16, 32)), (2, (512, 8, 16))])
 def test_fused_ipc_two_processes_bitwise(tmp_path, world, n):
-    """n = (256, ...) runs the x pass through the warp-per-line ring, whose TMA
+    """n = (512, ...) runs the x pass through the warp-per-line ring, whose TMA
     stores then target the other process's IPC-mapped buffer."""
     from paper_1309_2451_b200 import propagator, qgrid
 

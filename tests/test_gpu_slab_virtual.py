@@ -134,8 +134,8 @@ def run_virtual_fused(grid, v, a0, P, steps, tables=0):
 @pytest.mark.parametrize("P,n", [(2, (32, 16, 32)), (4, (32, 16, 32)), (8, (32, 16, 32)),
                                  (2, (256, 16, 16)), (8, (256, 16, 16)), (4, (512, 8, 16))])
 def test_fused_transport_bitwise_equal_single_gpu(P, n):
-    """nx = 256 / 512 run the x pass through the warp-per-line ring with TMA
-    stores into the peers' buffers; smaller nx through tile_kernel's peer stores."""
+    """nx = 512 runs the x pass through the warp-per-line ring with TMA stores
+    into the peers' buffers; other nx through tile_kernel's peer stores."""
     grid, v, a0 = _case(n)
     got = run_virtual_fused(grid, v, a0, P, 6)
     psi = qgrid.Wavefunction(a0.copy(), grid)
