@@ -8,8 +8,23 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ctap_internal.h"
 #include "ctap_sincos_tab.h"
+
+namespace {
+// NVTX range over one ABI call (header-only NVTX 3: a no-op unless a tool such
+// as nsys is attached), so device timelines show segments and passes by name
+struct Range {
+  explicit Range(const char* fmt, long long v = 0) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, fmt, v);
+    nvtxRangePushA(buf);
+  }
+  ~Range() { nvtxRangePop(); }
+};
+}  // namespace
 
 cudaError_t ctap_run_observe(const ctap_plan* p, const void* psi, const double* xs, const double* xb1,
                              const double* xb2, int margin, double* out, cudaStream_t st);
@@ -252,6 +267,7 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
 }
 
 CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, void* stream) {
+  Range nvtx("ctap_pass %lld", kind);
   if (!p || !in || !out) return fail(CTAP_EINVAL, "null argument");
   const bool diag = kind == ctap::PASS_Y_COPY || kind == ctap::PASS_X_COPY || kind == ctap::PASS_XB_COPY ||
                     kind == ctap::PASS_XP_COPY || kind == ctap::PASS_XP_KIN || (kind >= ctap::PASS_WX_COPY && kind <= ctap::PASS_WY_FWD);
@@ -320,6 +336,7 @@ static cudaError_t kin_block(ctap_plan* p, void* psi, cudaStream_t st) {
 }
 
 CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
+  Range nvtx("ctap_advance %lld steps", (long long)n);
   if (!p || !psi) return fail(CTAP_EINVAL, "null argument");
   if (n < 0) return fail(CTAP_EINVAL, "n_steps must be >= 0");
   if (p->slab_p != 1) return fail(CTAP_EINVAL, "ctap_advance drives single-GPU plans; use ctap_pass for slabs");
