@@ -161,10 +161,14 @@ __global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::
 #ifndef CTAP_TILE_E
 #define CTAP_TILE_E 8
 #endif
+#ifndef CTAP_E1024
+#define CTAP_E1024 8  // 16 measured: y passes equal, [x K x^-1] 7.70 -> 8.32 ms at 1024^2 x 512
+#endif
 
 template <int L, typename CV, int W>
 struct TileCfg {
-  static constexpr int E = (L >= 256) ? CTAP_TILE_E : kElems;
+  // 1024-point lines in 4-column tiles: 16 points per thread (64 threads per column)
+  static constexpr int E = (L >= 1024 && W == 4) ? CTAP_E1024 : (L >= 256) ? CTAP_TILE_E : kElems;
   static constexpr int T = L / E;
   static constexpr int per_tile = T * W;
   static constexpr int G = per_tile >= 128 ? 1 : 128 / per_tile;  // tiles per block
@@ -282,6 +286,17 @@ static cudaError_t dispatch_tile(int L, bool c64, const TileArgs& a, Tw tw, cuda
        : launch_tile<LL, KIND, PIN, POUT, KTAB, double2, W, PEERS>(a, tw.d, st))
   CTAP_BY_LENGTH(L, CTAP_T)
 #undef CTAP_T
+}
+
+// z columns per strided tile at L = 1024 (CTAP_W1024): 4 (default) keeps a
+// tile at 64 KB so two blocks fit per SM -- 1024^2 x 512: y passes 5.09 -> 4.17
+// ms, [x K x^-1] 8.16 -> 7.70 ms against 8-column tiles (bitwise equal)
+static int w1024() {
+  static const int w = [] {
+    const char* e = getenv("CTAP_W1024");
+    return e ? atoi(e) : 4;
+  }();
+  return w;
 }
 
 static int ilog2(int64_t v) {
@@ -623,6 +638,13 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
       a.lin = y_nat;
       a.lout = y_nat;
       const bool fwd = (kind == PASS_Y_FWD || kind == PASS_Y_FWD_TO_PEER);
+      if (L == 1024 && w1024() == 4 && !zsub && nz % 4 == 0) {  // 4-column tiles (64 KB): 2 blocks per SM
+        a.nchunk = (uint32_t)(nz / 4);
+        if (c64) return fwd ? launch_tile<1024, T_FWD, false, false, false, float2, 4>(a, tw.f, st)
+                            : launch_tile<1024, T_INV, false, false, false, float2, 4>(a, tw.f, st);
+        return fwd ? launch_tile<1024, T_FWD, false, false, false, double2, 4>(a, tw.d, st)
+                   : launch_tile<1024, T_INV, false, false, false, double2, 4>(a, tw.d, st);
+      }
       if (use_tma && (c64 || tma_mode == 3) && in == out) {  // measured: faster for complex64 only
         cudaError_t e = ctap_run_tma_pass(p, 1, fwd ? T_FWD : T_INV, out, a, st);
         if (e != cudaErrorNotSupported) return e;
@@ -693,6 +715,11 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
         const int tk = kind == PASS_X_KIN ? T_KIN : kind == PASS_X_FWD ? T_FWD : T_INV;
         cudaError_t e = ctap_run_tma_pass(p, 2, tk, out, a, st);
         if (e != cudaErrorNotSupported) return e;
+      }
+      if (L == 1024 && w1024() == 4 && kind == PASS_X_KIN && !p->expk_dev && nz % 4 == 0) {
+        a.nchunk = (uint32_t)(nz / 4);
+        return c64 ? launch_tile<1024, T_KIN, false, false, false, float2, 4>(a, tw.f, st)
+                   : launch_tile<1024, T_KIN, false, false, false, double2, 4>(a, tw.d, st);
       }
       if (xw16) {  // 16-column tiles: 256-byte rows for the large-stride x lines
         a.nchunk = (uint32_t)(nz / 16);

@@ -304,3 +304,33 @@ def test_wline_bitwise_equals_tile_kernel(monkeypatch, n):
         ref = run("0", kind)
         for mode in modes:
             assert np.array_equal(run(mode, kind), ref)
+
+
+def test_1024_line_tiles_bitwise(tmp_path):
+    """1024-point y and x lines run in 4-column tiles by default
+    (CTAP_W1024=4, two 64 KB tiles per SM); the transform is the same, so the
+    8-column tiles (CTAP_W1024=8) give identical bits.  CTAP_W1024 is read once
+    per process, so each variant runs in its own subprocess."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np\n"
+        "from paper_1309_2451_b200 import propagator, qgrid\n"
+        "from paper_1309_2451_b200.constants import species_mass\n"
+        "n = (1024, 16, 32)\n"
+        "g = qgrid.make_grid(*n, (20e-6, 4e-6, 250e-6), origin=(-10e-6, 1.25e-7, 0.0))\n"
+        "r = np.random.default_rng(2)\n"
+        "v = 1e-30 * (1 + r.random(n))\n"
+        "w = qgrid.Wavefunction(r.standard_normal(n) + 1j * r.standard_normal(n), g)\n"
+        "w, _ = propagator.evolve_real(w, propagator.make_plan(g, v, species_mass('li6'), 1e-6), 10)\n"
+        "np.save(sys.argv[1], w.amplitudes)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for w in ("4", "8"):
+        path = str(tmp_path / f"w{w}.npy")
+        subprocess.run([sys.executable, "-c", code, path], check=True, cwd=root,
+                       env=dict(os.environ, CTAP_W1024=w, PYTHONPATH=root))
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
