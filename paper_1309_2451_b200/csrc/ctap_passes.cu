@@ -638,6 +638,12 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
       a.lin = y_nat;
       a.lout = y_nat;
       const bool fwd = (kind == PASS_Y_FWD || kind == PASS_Y_FWD_TO_PEER);
+      if (L == 1024 && !c64 && !zsub && in == out && p->wline) {
+        // 1024-point y lines: warp-per-line ring (4-column tiles, two warps
+        // per column) -- 2.85 vs 4.25 ms at 1024^2 x 512 (ctap_wline.cu)
+        cudaError_t e = ctap_run_wline(p, 1, fwd ? T_FWD : T_INV, p->wline, out, a, st);
+        if (e != cudaErrorNotSupported) return e;
+      }
       if (L == 1024 && w1024() == 4 && !zsub && nz % 4 == 0) {  // 4-column tiles (64 KB): 2 blocks per SM
         a.nchunk = (uint32_t)(nz / 4);
         if (c64) return fwd ? launch_tile<1024, T_FWD, false, false, false, float2, 4>(a, tw.f, st)

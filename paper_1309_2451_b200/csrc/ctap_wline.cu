@@ -90,14 +90,23 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Column c of a [row][8] complex128 tile with the 128-byte XOR swizzle
-// (identical to TMA's CU_TENSOR_MAP_SWIZZLE_128B on a 1 KB aligned buffer).
-struct SwzCol {
+// Column c of a [row][W] complex128 tile with the TMA XOR swizzle of its row
+// width (W = 8: 128-byte rows, CU_TENSOR_MAP_SWIZZLE_128B, 16-byte chunk
+// c ^ (i & 7); W = 4: 64-byte rows, SWIZZLE_64B, chunk c ^ ((i >> 1) & 3)) on a
+// 1 KB aligned buffer.  Either way the bank group of element i is a bijection
+// of i & 7, so 8 consecutive rows never conflict, and at(e) -- the FFT
+// exchange view permuted by sigma(e) = e ^ ((e >> 3) & 7) -- keeps every
+// radix-8 scatter and gather conflict free.
+template <int W = 8>
+struct SwzColT {
   double2* buf;
   int c;
-  __device__ __forceinline__ double2& nat(int i) const { return buf[i * 8 + (c ^ (i & 7))]; }
+  __device__ __forceinline__ double2& nat(int i) const {
+    return W == 8 ? buf[i * 8 + (c ^ (i & 7))] : buf[i * 4 + (c ^ ((i >> 1) & 3))];
+  }
   __device__ __forceinline__ double2& at(int e) const { return nat(e ^ ((e >> 3) & 7)); }
 };
+using SwzCol = SwzColT<8>;
 
 // exp(-i k^2 dt/2)/N (real time: (cos, sin); imaginary time: (decay, 0)),
 // the recipe of mul_kphase (ctap_tile.cuh)
@@ -171,8 +180,8 @@ __device__ __forceinline__ void column(const SwzCol& col, int lane, const double
 // 16 warps while two tiles load.  The kx-mirror factors cross the two warps,
 // so they are exchanged through the column's own slots (indices < L/2,
 // free between the transforms).
-template <int L, int KIND>
-__device__ __forceinline__ void column2(const SwzCol& col, int ct, const double2* __restrict__ tw,
+template <int L, int KIND, typename Col>
+__device__ __forceinline__ void column2(const Col& col, int ct, const double2* __restrict__ tw,
                                         const PhaseArgs& ph, uint32_t o, uint32_t z, SyncNamed sync) {
   constexpr int E = L / 64;
   static_assert(E >= 8, "two warps per column need L >= 512 (radix-8 stages)");
@@ -233,12 +242,12 @@ struct NoPeers {};
 // AXIS 1 / 2: y / x lines of the natural layout (in place); AXIS 4: x lines of
 // the slab's y-slab, results stored by TMA straight into the other ranks'
 // buffers (the transpose of the fused slab transport).
-template <int L, int KIND, int AXIS, typename PM, int WPC = 1>
+template <int L, int KIND, int AXIS, typename PM, int WPC = 1, int W = kCols>
 __global__ void __launch_bounds__(kRingThreads, 1)
     ring_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a, const double2* __restrict__ tw,
                 const __grid_constant__ PM pm) {
   constexpr int BOX = L < 256 ? L : 256;
-  constexpr uint32_t kTileBytes = (uint32_t)L * kCols * sizeof(double2);
+  constexpr uint32_t kTileBytes = (uint32_t)L * W * sizeof(double2);
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // swizzle atom: 1 KB
   double2* bufs = reinterpret_cast<double2*>(base);
@@ -251,22 +260,22 @@ __global__ void __launch_bounds__(kRingThreads, 1)
   auto coords = [&](uint32_t j, int& c0, int& o) {
     const uint32_t tile = blockIdx.x + j * gridDim.x;
     const uint32_t oo = tile / a.nchunk;
-    c0 = (int)((tile - oo * a.nchunk) * 16);  // 8 complex = 16 scalars per column block
+    c0 = (int)((tile - oo * a.nchunk) * 2 * W);  // W complex = 2W scalars per column block
     o = (int)oo;
   };
   auto load = [&](uint32_t j) {
     const int b = j % kBufs;
-    double2* buf = bufs + (size_t)b * L * kCols;
+    double2* buf = bufs + (size_t)b * L * W;
     int c0, o;
     coords(j, c0, o);
     fence_async_smem();
     bar_expect_tx(&full[b], kTileBytes);
 #pragma unroll
     for (int q = 0; q < L / BOX; ++q)
-      tma_load(buf + q * BOX * kCols, &tmap, &full[b], c0, AXIS != 1 ? o : q * BOX, AXIS != 1 ? q * BOX : o);
+      tma_load(buf + q * BOX * W, &tmap, &full[b], c0, AXIS != 1 ? o : q * BOX, AXIS != 1 ? q * BOX : o);
   };
 
-  constexpr int kWarpsPerTile = kCols * WPC;           // WPC 2: all 16 warps on one tile
+  constexpr int kWarpsPerTile = W * WPC;  // (8, 1) or (4, 2): 2 groups; (8, 2): all 16 warps on one tile
   constexpr int kTileGroups = kGroups * kCols / kWarpsPerTile;
   if (threadIdx.x == 0) {
     for (int b = 0; b < kBufs; ++b) {
@@ -289,12 +298,12 @@ __global__ void __launch_bounds__(kRingThreads, 1)
     bar_wait(&full[b], k & 1);
     const uint32_t tile = blockIdx.x + j * gridDim.x;
     const uint32_t o = tile / a.nchunk;
-    const uint32_t z = (tile - o * a.nchunk) * 8 + c;
-    double2* buf = bufs + (size_t)b * L * kCols;
+    const uint32_t z = (tile - o * a.nchunk) * W + c;
+    double2* buf = bufs + (size_t)b * L * W;
     if constexpr (WPC == 1) {
       column<L, KIND>(SwzCol{buf, c}, lane, tw, a.ph, o, z);
     } else {
-      column2<L, KIND>(SwzCol{buf, c}, (warp & 1) * 32 + lane, tw, a.ph, o, z, SyncNamed{1 + c, 64});
+      column2<L, KIND>(SwzColT<W>{buf, c}, (warp & 1) * 32 + lane, tw, a.ph, o, z, SyncNamed{1 + warp / 2, 64});
     }
     fence_async_smem();  // generic-proxy writes -> the TMA store
     __syncwarp();
@@ -313,11 +322,11 @@ __global__ void __launch_bounds__(kRingThreads, 1)
         if constexpr (AXIS == 4) {
           const int nxl = L / pm.P, bx = nxl < BOX ? nxl : BOX;
           for (int q = 0; q < pm.P; ++q)
-            for (int r0 = 0; r0 < nxl; r0 += bx) tma_store(&pm.m[q], buf + (q * nxl + r0) * kCols, c0, oo, r0);
+            for (int r0 = 0; r0 < nxl; r0 += bx) tma_store(&pm.m[q], buf + (q * nxl + r0) * W, c0, oo, r0);
         } else {
 #pragma unroll
           for (int q = 0; q < L / BOX; ++q)
-            tma_store(&tmap, buf + q * BOX * kCols, c0, AXIS == 2 ? oo : q * BOX, AXIS == 2 ? q * BOX : oo);
+            tma_store(&tmap, buf + q * BOX * W, c0, AXIS == 2 ? oo : q * BOX, AXIS == 2 ? q * BOX : oo);
         }
         bulk_commit();
         bulk_wait_read0();  // the buffer may be refilled once the store has read it
@@ -401,25 +410,28 @@ static int sm_count() {
 template <int L, int KIND, int AXIS>
 static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw, cudaStream_t st, int wpc = 1) {
   constexpr int BOX = L < 256 ? L : 256;
+  // 1024-point lines: 4-column tiles (64 KB), two warps per column
+  constexpr int W = L >= 1024 ? 4 : kCols;
+  if (L >= 1024) wpc = 2;
   EncodeTiledFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
-  const uint64_t nz2 = (uint64_t)a.nchunk * 8 * 2;  // scalars per z line
+  const uint64_t nz2 = (uint64_t)a.nchunk * W * 2;  // scalars per z line
   const uint64_t d1 = AXIS == 2 ? a.n_outer : L, d2 = AXIS == 2 ? L : a.n_outer;
   CUtensorMap map;
   std::memset(&map, 0, sizeof map);
   const cuuint64_t dims[3] = {nz2, d1, d2};
   const cuuint64_t strides[2] = {nz2 * sizeof(double), nz2 * sizeof(double) * d1};
-  const cuuint32_t box[3] = {16, AXIS == 2 ? 1u : (cuuint32_t)BOX, AXIS == 2 ? (cuuint32_t)BOX : 1u};
+  const cuuint32_t box[3] = {2 * W, AXIS == 2 ? 1u : (cuuint32_t)BOX, AXIS == 2 ? (cuuint32_t)BOX : 1u};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, data, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, W == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  auto k = ring_kernel<L, KIND, AXIS, NoPeers, 1>;
-  if constexpr (L >= 512 && KIND == T_KIN)
-    if (wpc == 2) k = ring_kernel<L, KIND, AXIS, NoPeers, 2>;
+  auto k = ring_kernel<L, KIND, AXIS, NoPeers, L >= 1024 ? 2 : 1, W>;
+  if constexpr (L == 512 && KIND == T_KIN)
+    if (wpc == 2) k = ring_kernel<L, KIND, AXIS, NoPeers, 2, W>;
   constexpr size_t smem =
-      (size_t)kBufs * L * kCols * sizeof(double2) + 2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t) + 1024;
+      (size_t)kBufs * L * W * sizeof(double2) + 2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t) + 1024;
   static cudaError_t init[2] = {cudaErrorNotReady, cudaErrorNotReady};
   cudaError_t& ini = init[wpc == 2 ? 1 : 0];
   if (ini == cudaErrorNotReady) ini = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -494,7 +506,7 @@ static cudaError_t launch_tile1(const TileArgs& a, void* data, const double2* tw
 
 using namespace ctap;
 
-// In-place strided pass on lines of length L = 256 or 512 through the
+// In-place strided pass on lines of length L = 256, 512 or 1024 through the
 // warp-per-line kernels: axis 2 = x lines of an (L, n_outer, nz) array
 // (kinds T_FWD, T_INV, T_KIN, T_COPY), axis 1 = y lines of an (n_outer, L, nz)
 // array (T_FWD, T_INV, T_COPY).  `mode` 1 ring, 2 tile, 3 ring with two warps
@@ -504,6 +516,26 @@ cudaError_t ctap_run_wline(const ctap_plan* p, int axis, int kind, int mode, voi
                            cudaStream_t st) {
   if (p->dtype != CTAP_C128 || mode < 1 || mode > 6) return cudaErrorNotSupported;
   const int64_t L = axis == 2 ? p->n[0] : p->n[1];
+  if (L == 1024) {  // 4-column tiles, two warps per column, ring only (diagnostic kinds too)
+    if (mode == 2 || mode == 5 || (axis == 1 && kind == T_KIN) || a.nchunk * 8 % 4) return cudaErrorNotSupported;
+    TileArgs b = a;
+    b.nchunk = a.nchunk * 2;  // the caller counts 8-column chunks
+    const double2* tw = p->twiddles + p->tw_off[7];
+    switch (kind) {
+      // x lines at 1024 have an 8 MiB stride: 64-byte TMA rows move them at
+      // ~2.3 TB/s (copy 7.4 ms at 1024^2 x 512), so [x K x^-1] stays on
+      // tile_kernel's 16-byte loads unless forced (CTAP_WLINE >= 4)
+      case T_KIN:
+        return axis == 2 && mode >= 4 ? wl::launch_ring<1024, T_KIN, 2>(b, data, tw, st) : cudaErrorNotSupported;
+      case T_FWD: return axis == 2 ? wl::launch_ring<1024, T_FWD, 2>(b, data, tw, st)
+                                   : wl::launch_ring<1024, T_FWD, 1>(b, data, tw, st);
+      case T_INV: return axis == 2 ? wl::launch_ring<1024, T_INV, 2>(b, data, tw, st)
+                                   : wl::launch_ring<1024, T_INV, 1>(b, data, tw, st);
+      case T_COPY: return axis == 2 ? wl::launch_ring<1024, T_COPY, 2>(b, data, tw, st)
+                                    : wl::launch_ring<1024, T_COPY, 1>(b, data, tw, st);
+    }
+    return cudaErrorNotSupported;
+  }
   if (L != 256 && L != 512) return cudaErrorNotSupported;
   // the 256-point kinetic pass stays on tile_kernel: with 8 points per lane
   // the ring measured slower there (0.158 vs 0.144 ms at 256^3); the

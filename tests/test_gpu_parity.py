@@ -276,7 +276,7 @@ def test_complex64_has_no_systematic_rounding_drift():
     assert rel_l2(out["complex64"][0], out["complex128"][0]) < 5e-5
 
 
-@pytest.mark.parametrize("n", [(512, 16, 32), (256, 32, 16)])
+@pytest.mark.parametrize("n", [(512, 16, 32), (256, 32, 16), (1024, 8, 16), (16, 1024, 16)])
 def test_wline_bitwise_equals_tile_kernel(monkeypatch, n):
     """The warp-per-line x-pass kernels (CTAP_WLINE=1 TMA ring, 2 one tile per
     CTA) use the same radix plan, twiddles and exact kinetic phase as
@@ -299,7 +299,7 @@ def test_wline_bitwise_equals_tile_kernel(monkeypatch, n):
                 psi = propagator.step(psi, plan)
         return psi.amplitudes
 
-    modes = ("1", "2", "3") if n[0] == 512 else ("4", "5", "6")  # 4-6: the ring also at nx = 256
+    modes = ("1", "2", "3") if n[0] == 512 or n[1] == 1024 else ("4", "5", "6")  # 4-6: forced ring (nx 256/1024)
     for kind in ("real_time", "imaginary_time"):
         ref = run("0", kind)
         for mode in modes:
