@@ -50,6 +50,10 @@ constexpr int kGroups = CTAP_WL_GROUPS;  // ring: tiles in computation at once
 constexpr int kBufs = 3;    // ring: tile buffers
 constexpr int kRingThreads = kGroups * kCols * 32;  // 2 groups: 16 warps, 4 per SM sub-partition, 128 registers each
 constexpr int kTileThreads = kCols * 32;
+#ifndef CTAP_FFT512
+#define CTAP_FFT512 1
+#endif
+constexpr bool kFft512 = CTAP_FFT512 != 0;  // specialised 512-point warp transform (fft512_warp)
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -128,6 +132,84 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src) {
   return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
+// The 512-point transform of one warp (16 points per lane) with the exchange
+// addresses of the swizzled, sigma-permuted column precomputed per lane: the
+// same stages, twiddles and butterflies as line_fft<512, DIR, 16> (bitwise
+// equal), without the generic per-access index arithmetic.  In 16-byte units,
+// with l7 = lane & 7 and u = r ^ l7, T(r) = 8 u + (c ^ u):
+//   stage-0 scatter (NS = 1): 64 j + T(r),                  j = lane + 32 b
+//   stage-1 scatter (NS = 8): 512 (j >> 3) + 64 r + T(r)
+//   gathers of e = lane + 32 m: 256 m + R(m & 1), R(p) = 8 S + (c ^ (S & 7)),
+//                               S = lane ^ ((lane >> 3) + 4 p)
+template <int DIR>
+__device__ __forceinline__ void fft512_warp(double2 (&v)[16], int lane, int c, const double2* __restrict__ tw,
+                                            double2* buf) {
+  using P = Plan<512, 16>;
+  const int l7 = lane & 7;
+  const int s0 = lane ^ (lane >> 3), s1 = lane ^ ((lane >> 3) + 4);
+  const double2* rd0 = buf + 8 * s0 + (c ^ (s0 & 7));
+  const double2* rd1 = buf + 8 * s1 + (c ^ (s1 & 7));
+  auto toff = [&](int r) {
+    const int u = r ^ l7;
+    return 8 * u + (c ^ u);
+  };
+  auto gather = [&]() {
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = (m & 1 ? rd1 : rd0)[256 * m];
+    __syncwarp();
+  };
+  // stage 0: radix 8, NS = 1 (no twiddles)
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    double2 u[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) u[r] = v[b + 2 * r];
+    Dft<8, DIR>::run(u);
+    double2* wb = buf + 64 * lane + 2048 * b;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) wb[toff(r)] = u[r];
+  }
+  gather();
+  // stage 1: radix 8, NS = 8, k = j & 7 = l7
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    double2 u[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) u[r] = v[b + 2 * r];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) u[r] = tw_mul<DIR>(u[r], __ldg(&tw[P::tw_offset(1) + (r - 1) * 8 + l7]));
+    Dft<8, DIR>::run(u);
+    double2* wb = buf + 512 * ((lane >> 3) + 4 * b);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) wb[64 * r + toff(r)] = u[r];
+  }
+  gather();
+  // stage 2 (last): radix 8, NS = 64, k = j = lane + 32 b; outputs stay in registers
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    double2 u[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) u[r] = v[b + 2 * r];
+    const int k = lane + 32 * b;
+#pragma unroll
+    for (int r = 1; r < 8; ++r) u[r] = tw_mul<DIR>(u[r], __ldg(&tw[P::tw_offset(2) + (r - 1) * 64 + k]));
+    Dft<8, DIR>::run(u);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[b + 2 * r] = u[r];
+  }
+}
+
+template <int L, int DIR>
+__device__ __forceinline__ void warp_fft(double2 (&v)[L / 32], int lane, const double2* __restrict__ tw,
+                                         const SwzCol& col) {
+  if constexpr (L == 512 && kFft512) {
+    fft512_warp<DIR>(v, lane, col.c, tw, col.buf);
+  } else {
+    line_fft<L, DIR, L / 32>(v, lane, tw, col, SyncWarp{});
+  }
+}
+
 // The warp's column: read (natural order), transform, write back.  o = outer
 // index (y of the x pass), z = the column's global z.
 template <int L, int KIND>
@@ -140,9 +222,9 @@ __device__ __forceinline__ void column(const SwzCol& col, int lane, const double
   __syncwarp();
   if constexpr (KIND == T_COPY) {  // diagnostics: the tile mover alone
   } else if constexpr (KIND == T_FWD) {
-    line_fft<L, -1, E>(v, lane, tw, col, SyncWarp{});
+    warp_fft<L, -1>(v, lane, tw, col);
   } else if constexpr (KIND == T_INV) {
-    line_fft<L, +1, E>(v, lane, tw, col, SyncWarp{});
+    warp_fft<L, +1>(v, lane, tw, col);
   } else {  // T_KIN
     double ky2, kz2;
     if (ph.kgen) {
@@ -152,7 +234,7 @@ __device__ __forceinline__ void column(const SwzCol& col, int lane, const double
       ky2 = __ldg(&ph.ky2[ph.outer_off + o]);
       kz2 = __ldg(&ph.kz2[ph.z_off + z]);
     }
-    line_fft<L, -1, E>(v, lane, tw, col, SyncWarp{});
+    warp_fft<L, -1>(v, lane, tw, col);
     // Lane t evaluates the factor of its point t + 32 q (q < E/2, index <
     // L/2).  Its point m = E - q has index L - ((32 - t) + 32 (q - 1)), the
     // mirror of lane 32 - t's point of iteration q - 1, received by shuffle;
@@ -169,7 +251,7 @@ __device__ __forceinline__ void column(const SwzCol& col, int lane, const double
     }
     const double2 fn = kfactor(kx2_of(L / 2, ph), ky2, kz2, ph);
     apply_k(v[E / 2], lane == 0 ? fn : shp, ph.imag);
-    line_fft<L, +1, E>(v, lane, tw, col, SyncWarp{});
+    warp_fft<L, +1>(v, lane, tw, col);
   }
 #pragma unroll
   for (int m = 0; m < E; ++m) col.nat(lane + 32 * m) = v[m];
