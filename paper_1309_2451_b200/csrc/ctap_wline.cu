@@ -149,10 +149,10 @@ __device__ __forceinline__ void fft512_warp(double2 (&v)[16], int lane, int c, c
   const int s0 = lane ^ (lane >> 3), s1 = lane ^ ((lane >> 3) + 4);
   const double2* rd0 = buf + 8 * s0 + (c ^ (s0 & 7));
   const double2* rd1 = buf + 8 * s1 + (c ^ (s1 & 7));
-  auto toff = [&](int r) {
-    const int u = r ^ l7;
-    return 8 * u + (c ^ u);
-  };
+  // T(r) = 8 u + (c ^ u) with u = r ^ l7; the two terms occupy disjoint bits,
+  // so T(r) = (9 r) ^ (9 l7 ^ c): one XOR with an immediate per scatter
+  const int tk = (9 * l7) ^ c;
+  auto toff = [&](int r) { return (9 * r) ^ tk; };
   auto gather = [&]() {
     __syncwarp();
 #pragma unroll
@@ -216,9 +216,11 @@ template <int L, int KIND>
 __device__ __forceinline__ void column(const SwzCol& col, int lane, const double2* __restrict__ tw,
                                        const PhaseArgs& ph, uint32_t o, uint32_t z) {
   constexpr int E = L / 32;
+  // element lane + 32 m of the column: row lane + 32 m, chunk c ^ (lane & 7)
+  double2* const nb = col.buf + 8 * lane + (col.c ^ (lane & 7));
   double2 v[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = col.nat(lane + 32 * m);
+  for (int m = 0; m < E; ++m) v[m] = nb[256 * m];
   __syncwarp();
   if constexpr (KIND == T_COPY) {  // diagnostics: the tile mover alone
   } else if constexpr (KIND == T_FWD) {
@@ -254,7 +256,7 @@ __device__ __forceinline__ void column(const SwzCol& col, int lane, const double
     warp_fft<L, +1>(v, lane, tw, col);
   }
 #pragma unroll
-  for (int m = 0; m < E; ++m) col.nat(lane + 32 * m) = v[m];
+  for (int m = 0; m < E; ++m) nb[256 * m] = v[m];
 }
 
 // The same transform with TWO warps per column (64 threads, E = L/64 points
