@@ -36,12 +36,12 @@ def test_nm_exports_only_the_abi():
     assert exported == declared_symbols()
 
 
-def _desc(n=(16, 16, 16), mode=0, p=1, r=0):
+def _desc(n=(16, 16, 16), mode=0, p=1, r=0, pc=0):
     d = _lib.CtapPlanDesc()
     for i in range(3):
         d.n[i] = n[i]
     d.e0, d.dt_i, d.len2, d.v_shift = 1.0, 1.0, 1e-12, 0.0
-    d.mode, d.slab_p, d.slab_r = mode, p, r
+    d.mode, d.slab_p, d.slab_r, d.pencil_c = mode, p, r, pc
     return d
 
 
@@ -51,6 +51,9 @@ def _desc(n=(16, 16, 16), mode=0, p=1, r=0):
     (dict(mode=7), _lib.CTAP_EINVAL, "unknown mode"),
     (dict(p=3), _lib.CTAP_EINVAL, "divisible"),
     (dict(p=2, r=2), _lib.CTAP_EINVAL, "out of range"),
+    (dict(p=6, pc=4), _lib.CTAP_EINVAL, "do not form a pencil grid"),
+    (dict(p=8, pc=4, n=(16, 16, 16)), _lib.CTAP_EINVAL, "pencil grid 2 x 4"),   # nz < 8 Pc
+    (dict(p=4, pc=2, r=4, n=(16, 16, 16)), _lib.CTAP_EINVAL, "out of range"),
 ])
 def test_plan_create_validation(kw, code, msg):
     import numpy as np
