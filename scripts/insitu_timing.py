@@ -27,6 +27,19 @@ def main():
     for _ in range(3):
         for _, k in seq:
             plan.native.run_pass(k, psi, psi)
+    def time_advance(label):
+        for _ in range(2):
+            plan.native.advance(psi, steps)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s0.record()
+        plan.native.advance(psi, steps)
+        s1.record()
+        torch.cuda.synchronize()
+        print(label, round(s0.elapsed_time(s1) / steps, 4), "ms/step")
+
+    if os.environ.get("INSITU_ADVANCE_FIRST"):
+        time_advance("advance first:")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4 * steps + 1)]
     torch.cuda.synchronize()
     ev[0].record()
@@ -54,15 +67,7 @@ def main():
         torch.cuda.synchronize()
         iso[n] = s0.elapsed_time(s1) / steps
     print("in isolation :", {n: round(t, 4) for n, t in iso.items()}, "sum", round(sum(iso.values()), 4))
-    for _ in range(2):
-        plan.native.advance(psi, steps)
-    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    s0.record()
-    plan.native.advance(psi, steps)
-    s1.record()
-    torch.cuda.synchronize()
-    print("advance      :", round(s0.elapsed_time(s1) / steps, 4), "ms/step")
+    time_advance("advance      :")
 
 
 if __name__ == "__main__":
