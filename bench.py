@@ -325,7 +325,9 @@ def run_ours(args):
             "data": "synthetic: paper-chip CTAP potential (device Biot-Savart, 9605 segments) and a Gaussian packet",
             "config": {"workload": "512^3 CTAP split-step propagation, complex128, dt = 1 us, Li-6 (BASELINE config 4)",
                        "grid": list(GRID_N), "extents_m": list(EXTENTS), "decomposition":
-                       f"x-slab x{world} ({prop.transport} transposes)" if world > 1 else "single GPU",
+                       (f"x-slab x{world} ({prop.transport} transposes)"
+                        + (f"; fused transport unavailable: {prop.transport_fallback}"
+                           if getattr(prop, "transport_fallback", None) else "")) if world > 1 else "single GPU",
                        "phase_factors": {0: "both on the fly (exact recipe)", 1: "exp(-iV dt) table, K on the fly",
                                          2: "K table, V on the fly", 3: "both tables"}[tables],
                        "bytes_per_point_step_actual": 128 + vtab + ktab,

@@ -183,36 +183,67 @@ class SlabPropagator:
         if transport not in ("nccl", "fused"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport if P > 1 else "nccl"
+        # why the fused transport was not used (None when it was, or not asked for)
+        self.transport_fallback = None
+        if self.transport == "fused" and not self._setup_fused(dt_):
+            self.transport = "nccl"
         if self.transport == "nccl":
             self.send = torch.empty(self.layout.points, dtype=dt_, device=dev)
             self.recv = torch.empty(self.layout.points, dtype=dt_, device=dev)
-        else:
-            self._setup_fused(dt_)
 
-    def _setup_fused(self, dtype):
+    def _setup_fused(self, dtype) -> bool:
         """Allocate this rank's y-slab and peer-major buffers, exchange CUDA IPC
-        handles with every rank and register the peer-mapped addresses."""
+        handles with every rank and register the peer-mapped addresses.
+
+        Collective and all-or-nothing: every rank reaches the same collectives
+        whatever fails locally, and if any rank cannot export or map a peer
+        buffer (no P2P path, IPC blocked) ALL ranks return False and the plan
+        uses the NCCL all-to-all transport instead (`transport_fallback` says
+        why).  Either transport computes bitwise the same slabs."""
         itemsize = 8 if dtype == torch.complex64 else 16
         nbytes = self.layout.points * itemsize
-        self.yslab = DeviceBuffer(nbytes)
-        self.peer = DeviceBuffer(nbytes)
-        mine = (self.yslab.ipc_handle(), self.peer.ipc_handle())
+        err = None
+        mine = None
+        try:
+            self.yslab = DeviceBuffer(nbytes)
+            self.peer = DeviceBuffer(nbytes)
+            mine = (self.yslab.ipc_handle(), self.peer.ipc_handle())
+        except Exception as e:  # noqa: BLE001 - reported to every rank below
+            err = f"rank {self.layout.rank}: {e}"
         handles = [None] * self.layout.P
         dist.all_gather_object(handles, mine, group=self.group)
         self._opened = []
         tabs = ([], [])
-        for q, (hy, hp) in enumerate(handles):
-            if q == self.layout.rank:
-                tabs[0].append(self.yslab.ptr)
-                tabs[1].append(self.peer.ptr)
-            else:
-                py, pp = open_ipc(hy), open_ipc(hp)
-                self._opened += [py, pp]
-                tabs[0].append(py)
-                tabs[1].append(pp)
-        self.native.set_peer_buffers(0, tabs[0])
-        self.native.set_peer_buffers(1, tabs[1])
+        if err is None and all(h is not None for h in handles):
+            try:
+                for q, (hy, hp) in enumerate(handles):
+                    if q == self.layout.rank:
+                        tabs[0].append(self.yslab.ptr)
+                        tabs[1].append(self.peer.ptr)
+                    else:
+                        py, pp = open_ipc(hy), open_ipc(hp)
+                        self._opened += [py, pp]
+                        tabs[0].append(py)
+                        tabs[1].append(pp)
+                self.native.set_peer_buffers(0, tabs[0])
+                self.native.set_peer_buffers(1, tabs[1])
+            except Exception as e:  # noqa: BLE001
+                err = f"rank {self.layout.rank}: {e}"
+        elif err is None:
+            err = "a peer rank could not export its buffers"
+        on_dev = dist.get_backend(self.group) == "nccl"
+        ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float32,
+                          device=self.v_local.device if on_dev else "cpu")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if ok.item() < 1.0:
+            self.transport_fallback = err or "a peer rank could not map the peer buffers"
+            for ptr in self._opened:
+                _lib.load().ctap_ipc_close(ctypes.c_void_p(ptr))
+            self._opened = []
+            self.yslab = self.peer = None
+            return False
         self._flag = torch.zeros(1, dtype=torch.float32, device=self.v_local.device)
+        return True
 
     def _barrier(self):
         # stream-ordered: every rank's preceding pass (and its system fence)

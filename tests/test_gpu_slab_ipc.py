@@ -87,3 +87,46 @@ def test_fused_ipc_two_processes_bitwise(tmp_path, world, n):
     s0, s1 = (np.load(f"{out}.{r}.sums.npy") for r in range(world))
     assert np.array_equal(s0, s1)  # rank-ordered combination: identical on every rank
     assert s0[0] * grid.dvol == pytest.approx(psi.norm(), rel=1e-13)
+
+
+def _fallback_worker(rank, world, port, out, fail_rank):
+    here = os.path.dirname(os.path.abspath(__file__))
+    for p in (here, os.path.dirname(here)):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1309_2451_b200 import slab
+
+        if rank == fail_rank:
+            def refuse(handle):
+                raise RuntimeError("peer mapping refused (test)")
+            slab.open_ipc = refuse
+        grid, v, a0, m = _case()
+        lay = slab.SlabLayout(grid.n, world, rank)
+        prop = slab.SlabPropagator(grid, torch.from_numpy(np.ascontiguousarray(v[lay.x_slice])).cuda(), m, 1e-6,
+                                   phase_tables=0, transport="fused")
+        with open(f"{out}.{rank}.txt", "w") as fh:
+            fh.write(f"{prop.transport}\n{prop.transport_fallback}\n{prop.send.numel()}")
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [0, 1])
+def test_fused_transport_falls_back_on_every_rank(tmp_path, fail_rank):
+    """One rank cannot map its peer's buffers: every rank (not just that one)
+    agrees on the NCCL all-to-all transport, so no rank is left waiting in a
+    collective the others never reach; the reason names the failing rank."""
+    out = str(tmp_path / "tr")
+    mp.spawn(_fallback_worker, args=(2, _port(), out, fail_rank), nprocs=2, join=True)
+    for r in range(2):
+        transport, why, n = open(f"{out}.{r}.txt").read().split("\n")
+        assert transport == "nccl"
+        assert int(n) == 16 * 16 * 32
+        if r == fail_rank:
+            assert "peer mapping refused" in why and f"rank {fail_rank}" in why
+        else:
+            assert why != "None"
