@@ -172,7 +172,9 @@ CTAP_API int ctap_v_sums(ctap_plan* plan, const void* psi_dev, double* out_dev, 
  * process: peer-mapped through ctap_ipc_open, or local) of every rank's
  * buffers: which = 0: the y-slab buffers (nx, ny/P, nz) the y pass writes;
  * which = 1: the peer-major buffers [P][nx/P][ny/P][nz] the x pass writes.
- * count must equal slab_p (<= 16). */
+ * count must equal slab_p (<= 16).  count 0 (ptrs may be NULL) unregisters
+ * both tables' entries of `which`: call it before closing the mappings, so a
+ * fused pass fails with CTAP_EINVAL instead of storing through a stale one. */
 CTAP_API int ctap_set_peer_buffers(ctap_plan* plan, int32_t which, void* const* ptrs, int32_t count);
 
 /* CUDA IPC helpers for the peer mapping: export a device allocation made by

@@ -10,6 +10,7 @@
 
 #include <nvtx3/nvToolsExt.h>
 
+#include "ctap_device.cuh"
 #include "ctap_internal.h"
 #include "ctap_sincos_tab.h"
 
@@ -176,17 +177,22 @@ CTAP_API int ctap_plan_create(const ctap_plan_desc* d, const double* kx2, const 
   if (const char* env = getenv("CTAP_ZCHUNK")) p->zchunk = atoll(env);
   if (p->zchunk % 8 || p->zchunk < 0 || (p->zchunk && d->n[2] % p->zchunk)) p->zchunk = 0;
   {  // sincos rotation tables: unscaled (V phases) and times 1/N (K phase)
-    std::vector<double> sc(4 * 256);
-    for (int k = 0; k < 256; ++k) {
-      sc[2 * k] = kSinCos256[k][0];
-      sc[2 * k + 1] = kSinCos256[k][1];
-      sc[512 + 2 * k] = kSinCos256[k][0] * p->inv_scale;  // exact: power of two
-      sc[512 + 2 * k + 1] = kSinCos256[k][1] * p->inv_scale;
+    // kSCN entries (cos, sin)(2 pi j / kSCN) = entry j 256/kSCN of the 256 table
+    std::vector<double> sc(4 * ctap::kSCN);
+    for (int j = 0; j < ctap::kSCN; ++j) {
+      const int k = j * (256 / ctap::kSCN);
+      sc[2 * j] = kSinCos256[k][0];
+      sc[2 * j + 1] = kSinCos256[k][1];
+      sc[2 * ctap::kSCN + 2 * j] = kSinCos256[k][0] * p->inv_scale;  // exact: power of two
+      sc[2 * ctap::kSCN + 2 * j + 1] = kSinCos256[k][1] * p->inv_scale;
     }
     if (e == cudaSuccess) e = cudaMalloc((void**)&p->sctab, sc.size() * sizeof(double));
     if (e == cudaSuccess) e = cudaMemcpy(p->sctab, sc.data(), sc.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
   std::vector<double> tw = ctap_make_twiddles(p->tw_off);
+  ctap_append_twiddles2(tw, p->tw2_off);
+  p->z2 = 0;  // measured slower at 512^3: opt-in
+  if (const char* env = getenv("CTAP_Z2")) p->z2 = atoi(env);
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->twiddles, tw.size() * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(p->twiddles, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {  // complex64 copy of the (correctly rounded) double table
@@ -431,10 +437,15 @@ CTAP_API int ctap_v_sums(ctap_plan* p, const void* psi, double* out, void* strea
 }
 
 CTAP_API int ctap_set_peer_buffers(ctap_plan* p, int32_t which, void* const* ptrs, int32_t count) {
-  if (!p || !ptrs) return fail(CTAP_EINVAL, "null argument");
+  if (!p) return fail(CTAP_EINVAL, "null argument");
   if (which != 0 && which != 1) return fail(CTAP_EINVAL, "which must be 0 (y-slab) or 1 (peer-major)");
-  if (count != p->slab_p || count > 16) return fail(CTAP_EINVAL, "expected %d peer buffers", p->slab_p);
   void** tab = which == 0 ? p->peer_y : p->peer_p;
+  if (count == 0) {  // unregister (before the mappings are closed): the fused passes then fail with EINVAL
+    for (int q = 0; q < 16; ++q) tab[q] = nullptr;
+    return CTAP_OK;
+  }
+  if (!ptrs) return fail(CTAP_EINVAL, "null argument");
+  if (count != p->slab_p || count > 16) return fail(CTAP_EINVAL, "expected %d peer buffers", p->slab_p);
   for (int q = 0; q < count; ++q) {
     if (!ptrs[q]) return fail(CTAP_EINVAL, "peer buffer %d is null", q);
     tab[q] = ptrs[q];

@@ -18,6 +18,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace ctap {
@@ -221,6 +222,27 @@ struct SyncNamed {  // T threads (a multiple of 32) of one line: named barrier
   }
 };
 
+// Twiddles of a complex128 radix-8 butterfly: u[r] *= w^r (w = exp(-2 pi i
+// k / (8 NS)), conjugated for DIR > 0).  Three table loads (w, w^2, w^4; the
+// table's column k at stride NS) and the other four as their products: the
+// axis passes are bound by the L1 data pipe (ncu r02), and a twiddle gather
+// costs up to 4 wavefronts against 4 FP64 instructions for a product.  The
+// products carry ~1 ulp more rounding than table values; FFT roundoff is not
+// what the 1e-10 parity gate is sensitive to.  Every radix-8
+// kernel uses this helper, so all of them stay bitwise interchangeable.
+template <int DIR>
+__device__ __forceinline__ void radix8_twiddles(double2* u, const double2* __restrict__ col, int NS) {
+  const double2 w1 = __ldg(col), w2 = __ldg(col + NS), w4 = __ldg(col + 3 * NS);
+  const double2 w3 = cmul(w1, w2);
+  u[1] = tw_mul<DIR>(u[1], w1);
+  u[2] = tw_mul<DIR>(u[2], w2);
+  u[3] = tw_mul<DIR>(u[3], w3);
+  u[4] = tw_mul<DIR>(u[4], w4);
+  u[5] = tw_mul<DIR>(u[5], cmul(w1, w4));
+  u[6] = tw_mul<DIR>(u[6], cmul(w2, w4));
+  u[7] = tw_mul<DIR>(u[7], cmul(w3, w4));
+}
+
 // One Stockham stage on the eight registers of thread t.
 //   radix R, stride Ns (product of earlier radices), line length L.
 // Input: v[m] = x[t + m*T].  Output scattered to smem (unless last stage, in
@@ -237,11 +259,15 @@ __device__ __forceinline__ void stockham_stage(C* v, int t, const TwOf<C>* __res
     const int j = t + b * T;
     const int k = j & (NS - 1);
     if (NS > 1) {
-      // twiddle exp(DIR 2 pi i r k / (NS R)) from the stage-major table
+      if constexpr (R == 8 && std::is_same<C, double2>::value) {
+        radix8_twiddles<DIR>(u, tw + TWO + k, NS);
+      } else {
+        // twiddle exp(DIR 2 pi i r k / (NS R)) from the stage-major table
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const TwOf<C> w = __ldg(&tw[TWO + (r - 1) * NS + k]);
-        u[r] = tw_mul<DIR>(u[r], w);
+        for (int r = 1; r < R; ++r) {
+          const TwOf<C> w = __ldg(&tw[TWO + (r - 1) * NS + k]);
+          u[r] = tw_mul<DIR>(u[r], w);
+        }
       }
     }
     Dft<R, DIR>::run(u);
@@ -308,57 +334,95 @@ __device__ __forceinline__ double k_phase(double kx2, double ky2, double kz2, do
 }
 
 
+// sincos rotation table size: 2^kSCBits entries (cos, sin)(2 pi j / 2^kSCBits)
+#ifndef CTAP_SC_BITS
+#define CTAP_SC_BITS 8
+#endif
+constexpr int kSCBits = CTAP_SC_BITS;
+constexpr int kSCN = 1 << kSCBits;
+static_assert(kSCBits == 4 || kSCBits == 8, "sincos table: 16 or 256 entries");
+
 // polynomial/reduction constants as constant-bank operands (no per-use
-// register materialisation)
-__constant__ double kSC[10] = {
-    40.74366543152521,         // 0: 128/pi
-    0x1.921fb54000000p-6,      // 1: pi/128 = C1 + C2 + C3 (27 + 27 + 53 bits)
-    0x1.10b4610000000p-36,     // 2
-    0x1.a62633145c06ep-64,     // 3
-    -1.9841269841269841e-04,   // 4: -1/7!
-    8.3333333333333333e-03,    // 5: 1/5!
-    -1.6666666666666666e-01,   // 6: -1/3!
-    -1.3888888888888889e-03,   // 7: -1/6!
-    4.1666666666666664e-02,    // 8: 1/4!
-    6755399441055744.0,        // 9: 1.5 * 2^52
+// register materialisation).  Step h = 2 pi / kSCN = C1 + C2 + C3 (27 + 27 +
+// 53 bits: n C1 is exact for |n| < 2^26), the pi/128 split scaled by a power
+// of two.
+__constant__ double kSC[16] = {
+    kSCN / 6.283185307179586476925286766559,  // 0: 1/h
+    0x1.921fb54000000p-6 * (256 / kSCN),      // 1: C1
+    0x1.10b4610000000p-36 * (256 / kSCN),     // 2: C2
+    0x1.a62633145c06ep-64 * (256 / kSCN),     // 3: C3
+    6755399441055744.0,                       // 4: 1.5 * 2^52
+    -1.6666666666666666e-01,                  // 5: -1/3!
+    8.3333333333333333e-03,                   // 6: 1/5!
+    -1.9841269841269841e-04,                  // 7: -1/7!
+    2.7557319223985893e-06,                   // 8: 1/9!
+    -2.5052108385441720e-08,                  // 9: -1/11!
+    -0.5,                                     // 10: -1/2!
+    4.1666666666666664e-02,                   // 11: 1/4!
+    -1.3888888888888889e-03,                  // 12: -1/6!
+    2.4801587301587302e-05,                   // 13: 1/8!
+    -2.7557319223985888e-07,                  // 14: -1/10!
+    0.0,
 };
+
+// the out-of-range path of fast_sincos, kept out of line: inlined at every
+// point of a kernel it would multiply the code size
+__device__ __noinline__ inline void slow_sincos(double phi, const double2* __restrict__ tab, double* s, double* c) {
+  double ss, cc;
+  sincos(phi, &ss, &cc);
+  const double f = __ldg(&tab[0].x);
+  *s = ss * f;
+  *c = cc * f;
+}
 
 // sincos for the phase factors.  The phase itself is exact (computed with the
 // recipes above); only cos/sin of it are evaluated here, to ~1.5 ulp:
-//   n = rint(phi * 128/pi) via the 1.5*2^52 magic constant, r = phi - n*pi/128
-//   by a three-term Cody-Waite split (exact first term for |n| < 2^26),
-//   Taylor polynomials on |r| <= pi/256 (sin to r^7, cos to r^6; the next
-//   terms are below 1e-20), and a rotation by tab[n & 255] = f (cos, sin)(n pi/128)
-//   where f is a per-plan factor (1, or the kinetic step's 1/N folded in -- a
-//   power of two, so the folding is exact).
-// 16 FP64 operations against ~40 FP64 + ~70 other instructions for the library
-// sincos; |phi| >= 2^20 falls back to the library (never on CTAP grids, where
+//   n = rint(phi / h) via the 1.5*2^52 magic constant, r = phi - n h by a
+//   three-term Cody-Waite split, Taylor polynomials on |r| <= h/2, and a
+//   rotation by tab[n mod kSCN] = f (cos, sin)(n h) where f is a per-plan
+//   factor (1, or the kinetic step's 1/N folded in -- a power of two, so the
+//   folding is exact).
+// With 256 entries (h = pi/128, the default) the polynomials stop at r^7 /
+// r^6; the kinetic phases (k^2 varies fast along a line) scatter a warp's
+// gather over ~30 128-byte lines.  With 16 entries (CTAP_SC_BITS=4: h = pi/8,
+// polynomials to r^11 / r^10, truncation < 1e-17) a gather touches at most two
+// lines, but the four extra FMAs cost more than the wavefronts they save:
+// [x K x^-1] 1.177 -> 1.210 ms, [z^-1 V z] 1.067 -> 1.077 ms (B200, r02).
+// |phi| >= 2^20 falls back to the library (never on CTAP grids, where
 // |phi| < 1e6) and applies f = tab[0].x explicitly.  Errors of an ulp in the
 // factor are harmless (only the phase must be bit-exact).
 __device__ __forceinline__ void fast_sincos(double phi, const double2* __restrict__ tab, double* s, double* c) {
   if (fabs(phi) < 1048576.0) {
-    const double t = fma(phi, kSC[0], kSC[9]);
+    const double t = fma(phi, kSC[0], kSC[4]);
     const int n = __double2loint(t);
-    const double nf = t - kSC[9];
+    const double nf = t - kSC[4];
     double r = fma(-nf, kSC[1], phi);
     r = fma(-nf, kSC[2], r);
     r = fma(-nf, kSC[3], r);
     const double r2 = r * r;
-    double ps = fma(r2, kSC[4], kSC[5]);
-    ps = fma(r2, ps, kSC[6]);
+    double ps, pc;
+    if constexpr (kSCBits == 4) {
+      ps = fma(r2, kSC[9], kSC[8]);
+      ps = fma(r2, ps, kSC[7]);
+      ps = fma(r2, ps, kSC[6]);
+      ps = fma(r2, ps, kSC[5]);
+      pc = fma(r2, kSC[14], kSC[13]);
+      pc = fma(r2, pc, kSC[12]);
+      pc = fma(r2, pc, kSC[11]);
+      pc = fma(r2, pc, kSC[10]);
+    } else {
+      ps = fma(r2, kSC[7], kSC[6]);
+      ps = fma(r2, ps, kSC[5]);
+      pc = fma(r2, kSC[12], kSC[11]);
+      pc = fma(r2, pc, kSC[10]);
+    }
     const double sr = fma(r * r2, ps, r);
-    double pc = fma(r2, kSC[7], kSC[8]);
-    pc = fma(r2, pc, -0.5);
     const double cr = fma(r2, pc, 1.0);
-    const double2 tb = __ldg(&tab[n & 255]);
+    const double2 tb = __ldg(&tab[n & (kSCN - 1)]);
     *c = fma(tb.x, cr, -(tb.y * sr));
     *s = fma(tb.y, cr, tb.x * sr);
   } else {
-    double ss, cc;
-    sincos(phi, &ss, &cc);
-    const double f = __ldg(&tab[0].x);
-    *s = ss * f;
-    *c = cc * f;
+    slow_sincos(phi, tab, s, c);
   }
 }
 

@@ -1,6 +1,7 @@
 // Internal plan object shared by the kernels and the C ABI (not exported).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -65,7 +66,7 @@ struct ctap_plan {
   void* expv_dev;          // optional table exp(-i v_i dt_i), plan precision (phase_tables, real time)
   void* expk_dev;          // optional table exp(-i k^2 dt/2) / N, x-pass layout
   double* k2_dev[3];       // squared wavenumbers per axis (global lengths)
-  double2* sctab;          // [256] (cos, sin)(k pi/128), [256] the same times 1/N
+  double2* sctab;          // [kSCN] (cos, sin)(2 pi j / kSCN), [kSCN] the same times 1/N (ctap_device.cuh)
   int kgen;                // k^2 regenerated on device from kval (tables verified)
   int wline;               // x-pass kernel: 1 warp-per-line ring, 2 warp-per-line tile, 0 tile_kernel
   int64_t zchunk;          // kinetic block in z chunks of this width (0: whole volume)
@@ -74,6 +75,8 @@ struct ctap_plan {
   double2* twiddles;       // stage-major twiddle tables for L = 8..1024
   float4* twiddles32;      // the same as float-float pairs (complex64 mode)
   int tw_off[8];           // start of the table of L = 8 << i
+  int tw2_off[5];          // start of the two-stage plan's stage-2 table of L = 64 << i (ctap_fft2.cuh)
+  int z2;                  // z passes on the two-stage FFT (complex128, nz >= 64); CTAP_Z2=0 disables
   double2* kbuf;           // single-GPU k-space buffer (blocked layout, out of place y passes)
   int k_lx;                // log2 of the x block of the k-space layout (0: natural)
   void* peer_y[16];        // fused slab transposes: every rank's y-slab buffer
@@ -95,6 +98,46 @@ cudaError_t ctap_run_phase_field(const ctap_plan* p, int which, void* out, cudaS
 cudaError_t ctap_run_phase_table(const ctap_plan* p, int which, void* out, cudaStream_t st);
 #include <vector>
 std::vector<double> ctap_make_twiddles(int off[8]);
+void ctap_append_twiddles2(std::vector<double>& t, int off2[5]);
+namespace ctap {
+struct ZArgs;
+}
+cudaError_t ctap_run_z2(const ctap_plan* p, int tkind, bool vtab, int ch, const ctap::ZArgs& a, cudaStream_t st);
+static inline int ilog2i(int64_t v) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return l;
+}
 cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* out, cudaStream_t st);
 cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* out, int64_t z0, int64_t zn,
                             cudaStream_t st);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute belongs to the function of the current device's context, so a
+// process that also launches on a second device must set it there too.
+// `done` is the call site's per-kernel bitmask of device ordinals.
+template <typename K>
+static inline cudaError_t ctap_smem_attr(K k, size_t bytes, std::atomic<uint64_t>& done) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.fetch_or(bit);
+  return e;
+}
+
+// multiprocessor count of the current device, cached per device ordinal
+static inline int ctap_sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}

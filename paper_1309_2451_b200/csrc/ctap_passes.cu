@@ -68,15 +68,6 @@ struct ZCfg {
   static constexpr size_t smem = (size_t)C * smem_line * sizeof(CV);
 };
 
-struct ZArgs {
-  void* psi;
-  uint32_t nlines;  // nx_local * ny
-  PhaseArgs ph;
-  // pencil z-chunked side (CH bit 0: input, bit 1: output): point z of line l
-  // at (z >> lzc) cs + l 2^lzc + (z & (2^lzc - 1)), cs = nlines 2^lzc
-  void* out;
-  uint32_t lzc, cs;
-};
 
 template <int L, int KIND, bool VTAB, typename CV, typename Sync>
 __device__ __forceinline__ void z_body(const ZArgs& a, CV* v, int t, uint32_t off, bool active,
@@ -105,9 +96,15 @@ __device__ __forceinline__ void z_body(const ZArgs& a, CV* v, int t, uint32_t of
     line_fft<L, -1>(v, t, tw, sm, sync);
   } else {  // T_VMID: inverse, V, forward; T_VLAST: inverse, Vh
     double vi[kElems];
+#ifndef CTAP_Z_VLATE
 #pragma unroll
     for (int m = 0; m < kElems; ++m) vi[m] = active ? __ldcg(&a.ph.vi[off + t + m * T]) : 0.0;
+#endif
     line_fft<L, +1>(v, t, tw, sm, sync);
+#ifdef CTAP_Z_VLATE
+#pragma unroll
+    for (int m = 0; m < kElems; ++m) vi[m] = active ? __ldcg(&a.ph.vi[off + t + m * T]) : 0.0;
+#endif
 #pragma unroll
     for (int m = 0; m < kElems; ++m) mul_vphase(v[m], vi[m], KIND == T_VMID ? -1.0 : -0.5, a.ph);
     if constexpr (KIND == T_VMID) line_fft<L, -1>(v, t, tw, sm, sync);
@@ -225,18 +222,13 @@ __global__ void __launch_bounds__(TileCfg<L, CV, W>::threads,
 // host-side dispatch
 // ---------------------------------------------------------------------------
 
-template <typename K>
-static cudaError_t allow_smem(K k, size_t bytes) {
-  return bytes > 48 * 1024 ? cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)
-                           : cudaSuccess;
-}
 
 template <int L, int KIND, bool VTAB, typename CV, int CH = 0>
 static cudaError_t launch_z(const ZArgs& a, const TwOf<CV>* tw, cudaStream_t st) {
   using Cfg = ZCfg<L, CV>;
   auto k = zline_kernel<L, KIND, VTAB, CV, CH>;
-  static cudaError_t init = allow_smem(k, Cfg::smem);
-  if (init != cudaSuccess) return init;
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = ctap_smem_attr(k, Cfg::smem, attr_done)) return e;
   k<<<(a.nlines + Cfg::C - 1) / Cfg::C, Cfg::threads, Cfg::smem, st>>>(a, tw);
   return cudaGetLastError();
 }
@@ -245,8 +237,8 @@ template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W, b
 static cudaError_t launch_tile(const TileArgs& a, const TwOf<CV>* tw, cudaStream_t st) {
   using Cfg = TileCfg<L, CV, W>;
   auto k = tile_kernel<L, KIND, PIN, POUT, KTAB, CV, W, PEERS>;
-  static cudaError_t init = allow_smem(k, Cfg::smem);
-  if (init != cudaSuccess) return init;
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = ctap_smem_attr(k, Cfg::smem, attr_done)) return e;
   const uint32_t ntiles = a.n_outer * a.nchunk;
   k<<<(ntiles + Cfg::G - 1) / Cfg::G, Cfg::threads, Cfg::smem, st>>>(a, tw);
   return cudaGetLastError();
@@ -471,7 +463,7 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
   ph.outer_off = 0;
   ph.kgen = p->kgen;
   ph.sct = p->sctab;
-  ph.sctk = p->sctab + 256;
+  ph.sctk = p->sctab + kSCN;
   ph.z_off = (uint32_t)z0;
   for (int i = 0; i < 3; ++i) {
     ph.kn[i] = (uint32_t)p->n[i];
@@ -492,6 +484,11 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
       a.lzc = (uint32_t)ilog2(zc);
       a.cs = a.nlines * zc;
       const Tw tw = twid(p, nz);
+      {  // two-stage z kernel (ctap_zline2.cu) where it applies
+        const int tk = kind == PASS_PZ_FIRST ? T_VFIRST : kind == PASS_PZ_MID ? T_VMID : T_VLAST;
+        cudaError_t e = ctap_run_z2(p, tk, false, kind == PASS_PZ_FIRST ? 2 : kind == PASS_PZ_MID ? 3 : 1, a, st);
+        if (e != cudaErrorNotSupported) return e;
+      }
       if (kind == PASS_PZ_FIRST) return dispatch_z<T_VFIRST, false, 2>((int)nz, c64, a, tw, st);
       if (kind == PASS_PZ_MID) return dispatch_z<T_VMID, false, 3>((int)nz, c64, a, tw, st);
       return dispatch_z<T_VLAST, false, 1>((int)nz, c64, a, tw, st);
@@ -538,6 +535,12 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
     a.ph = ph;
     const Tw tw = twid(p, nz);
     const int L = (int)nz;
+    {  // two-stage z kernel (ctap_zline2.cu) where it applies
+      const int tk = kind == PASS_Z_FWD ? T_FWD : kind == PASS_Z_INV ? T_INV : kind == PASS_Z_FIRST ? T_VFIRST
+                     : kind == PASS_Z_MID ? T_VMID : T_VLAST;
+      cudaError_t e = ctap_run_z2(p, tk, p->expv_dev != nullptr, 0, a, st);
+      if (e != cudaErrorNotSupported) return e;
+    }
     switch (kind) {
       case PASS_Z_FWD: return dispatch_z<T_FWD, false>(L, c64, a, tw, st);
       case PASS_Z_INV: return dispatch_z<T_INV, false>(L, c64, a, tw, st);
@@ -722,7 +725,7 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
         cudaError_t e = ctap_run_tma_pass(p, 2, tk, out, a, st);
         if (e != cudaErrorNotSupported) return e;
       }
-      if (L == 1024 && w1024() == 4 && kind == PASS_X_KIN && !p->expk_dev && nz % 4 == 0) {
+      if (L == 1024 && w1024() == 4 && kind == PASS_X_KIN && !p->expk_dev && !zsub && nz % 4 == 0) {
         a.nchunk = (uint32_t)(nz / 4);
         return c64 ? launch_tile<1024, T_KIN, false, false, false, float2, 4>(a, tw.f, st)
                    : launch_tile<1024, T_KIN, false, false, false, double2, 4>(a, tw.d, st);

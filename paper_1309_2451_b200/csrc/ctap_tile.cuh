@@ -31,6 +31,17 @@ struct PhaseArgs {
   double kval[3];
 };
 
+// arguments of the z passes (contiguous lines)
+struct ZArgs {
+  void* psi;
+  uint32_t nlines;  // nx_local * ny
+  PhaseArgs ph;
+  // pencil z-chunked side (CH bit 0: input, bit 1: output): point z of line l
+  // at (z >> lzc) cs + l 2^lzc + (z & (2^lzc - 1)), cs = nlines 2^lzc
+  void* out;
+  uint32_t lzc, cs;
+};
+
 // squared angular wavenumber of FFT index i on an axis of n points with
 // 1/(n d) = val, formed as numpy's 2*pi*fftfreq(n, d) then squared
 // (qgrid.py k_axis / k_squared): ((2 pi) * (m * val))^2, m the signed index
@@ -134,10 +145,13 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, CV* v, int t, uint3
     double ky2 = 0.0, kz2 = 0.0;
     CV f[KTAB ? E : 1];
     if constexpr (KTAB) {
+      // expk spans the full nz: a z-chunked pass (a.out offset by z_off
+      // columns) indexes it at the chunk's absolute column
       const CV* expk = (const CV*)a.ph.expk;
 #pragma unroll
       for (int m = 0; m < E; ++m)
-        f[m] = active ? __ldcg(&expk[outer(a.lout, o) + inner<KBLK>(a.lout, t + m * T) + z]) : CT<CV>::mk(0, 0);
+        f[m] = active ? __ldcg(&expk[outer(a.lout, o) + inner<KBLK>(a.lout, t + m * T) + a.ph.z_off + z])
+                      : CT<CV>::mk(0, 0);
     } else if (a.ph.kgen) {
       ky2 = k2_gen(a.ph.outer_off + o, a.ph.kn[1], a.ph.kval[1]);
       kz2 = k2_gen(a.ph.z_off + z, a.ph.kn[2], a.ph.kval[2]);

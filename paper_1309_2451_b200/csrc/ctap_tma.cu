@@ -186,14 +186,9 @@ static cudaError_t launch_tma(const TileArgs& a, void* data, uint64_t d1, uint64
   if constexpr (!Cfg::ok) return cudaErrorNotSupported;
   auto k = tma_tile_kernel<L, KIND, CV, AXIS>;
   const size_t smem = Cfg::smem;
-  static cudaError_t init = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (init != cudaSuccess) return init;
-  static int sms = [] {
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-  }();
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = ctap_smem_attr(k, smem, attr_done)) return e;
+  const int sms = ctap_sm_count();
   const uint32_t ntiles = a.n_outer * a.nchunk;
   const uint32_t grid = ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms;
   k<<<grid, L * Cfg::G, smem, st>>>(map, a, tw);

@@ -177,8 +177,7 @@ __device__ __forceinline__ void fft512_warp(double2 (&v)[16], int lane, int c, c
     double2 u[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) u[r] = v[b + 2 * r];
-#pragma unroll
-    for (int r = 1; r < 8; ++r) u[r] = tw_mul<DIR>(u[r], __ldg(&tw[P::tw_offset(1) + (r - 1) * 8 + l7]));
+    radix8_twiddles<DIR>(u, tw + P::tw_offset(1) + l7, 8);
     Dft<8, DIR>::run(u);
     double2* wb = buf + 512 * ((lane >> 3) + 4 * b);
 #pragma unroll
@@ -192,8 +191,7 @@ __device__ __forceinline__ void fft512_warp(double2 (&v)[16], int lane, int c, c
 #pragma unroll
     for (int r = 0; r < 8; ++r) u[r] = v[b + 2 * r];
     const int k = lane + 32 * b;
-#pragma unroll
-    for (int r = 1; r < 8; ++r) u[r] = tw_mul<DIR>(u[r], __ldg(&tw[P::tw_offset(2) + (r - 1) * 64 + k]));
+    radix8_twiddles<DIR>(u, tw + P::tw_offset(2) + k, 64);
     Dft<8, DIR>::run(u);
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[b + 2 * r] = u[r];
@@ -479,15 +477,7 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-static int sm_count() {
-  static int sms = [] {
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-  }();
-  return sms;
-}
+static int sm_count() { return ctap_sm_count(); }
 
 // AXIS 2: x lines of an (L, n_outer, nz) array; AXIS 1: y lines of an
 // (n_outer, L, nz) array (nz = 8 * a.nchunk)
@@ -516,10 +506,8 @@ static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw,
     if (wpc == 2) k = ring_kernel<L, KIND, AXIS, NoPeers, 2, W>;
   constexpr size_t smem =
       (size_t)kBufs * L * W * sizeof(double2) + 2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t) + 1024;
-  static cudaError_t init[2] = {cudaErrorNotReady, cudaErrorNotReady};
-  cudaError_t& ini = init[wpc == 2 ? 1 : 0];
-  if (ini == cudaErrorNotReady) ini = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (ini != cudaSuccess) return ini;
+  static std::atomic<uint64_t> attr_done[2];
+  if (cudaError_t e = ctap_smem_attr(k, smem, attr_done[wpc == 2 ? 1 : 0])) return e;
   const uint32_t ntiles = a.n_outer * a.nchunk;
   const uint32_t grid = ntiles < (uint32_t)sm_count() ? ntiles : (uint32_t)sm_count();
   k<<<grid, kRingThreads, smem, st>>>(map, a, tw, NoPeers{});
@@ -563,8 +551,8 @@ static cudaError_t launch_ring_peers(const TileArgs& a, const void* in, int P, c
   auto k = ring_kernel<L, T_KIN, 4, PeerMaps>;
   constexpr size_t smem =
       (size_t)kBufs * L * kCols * sizeof(double2) + 2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t) + 1024;
-  static cudaError_t init = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (init != cudaSuccess) return init;
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = ctap_smem_attr(k, smem, attr_done)) return e;
   const uint32_t ntiles = a.n_outer * a.nchunk;
   const uint32_t grid = ntiles < (uint32_t)sm_count() ? ntiles : (uint32_t)sm_count();
   k<<<grid, kRingThreads, smem, st>>>(map, a, tw, pm);
@@ -579,8 +567,8 @@ static cudaError_t launch_tile1(const TileArgs& a, void* data, const double2* tw
   s.os = AXIS == 2 ? nz : (uint32_t)L * nz;
   auto k = tile1_kernel<L, KIND>;
   constexpr size_t smem = (size_t)L * kCols * sizeof(double2);
-  static cudaError_t init = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (init != cudaSuccess) return init;
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = ctap_smem_attr(k, smem, attr_done)) return e;
   k<<<a.n_outer * a.nchunk, kTileThreads, smem, st>>>((double2*)data, s, a, tw);
   return cudaGetLastError();
 }

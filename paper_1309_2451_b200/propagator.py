@@ -107,6 +107,12 @@ class NativePlan:
         arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
         _lib.call("ctap_set_peer_buffers", self.handle, int(which), arr, len(ptrs))
 
+    def clear_peer_buffers(self):
+        """Unregister both peer tables (count 0): the fused passes then fail
+        with EINVAL instead of storing through stale mappings."""
+        for which in (0, 1):
+            _lib.call("ctap_set_peer_buffers", self.handle, which, None, 0)
+
     def fft3d(self, data: torch.Tensor, direction: int = -1):
         _lib.call("ctap_fft3d", self.handle, data.data_ptr(), int(direction), _device.stream_handle())
 

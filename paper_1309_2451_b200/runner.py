@@ -13,6 +13,7 @@ the same attributes); manifests, CSV export and the CLI are out of scope.
 
 from __future__ import annotations
 
+import copy
 import dataclasses
 import os
 from dataclasses import dataclass
@@ -182,7 +183,11 @@ def run_sweep(cfg, out_dir=None, group=None, run_point=None) -> list:
     mine = {}
     for k in rank_share(len(points), rank, world):
         ordering, i_m = points[k]
-        cfg_point = dataclasses.replace(cfg, ordering=ordering) if dataclasses.is_dataclass(cfg) else cfg
+        if dataclasses.is_dataclass(cfg):
+            cfg_point = dataclasses.replace(cfg, ordering=ordering)
+        else:  # any object with the same attributes: a copy with this point's ordering
+            cfg_point = copy.copy(cfg)
+            setattr(cfg_point, "ordering", ordering)
         mine[k] = float(run_point(cfg_point, i_m))
     if dist_on:
         parts = [None] * world

@@ -237,6 +237,9 @@ class SlabPropagator:
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
         if ok.item() < 1.0:
             self.transport_fallback = err or "a peer rank could not map the peer buffers"
+            # unregister before unmapping: no plan keeps a peer address of a
+            # closed mapping (the fused passes then fail loudly instead)
+            self.native.clear_peer_buffers()
             for ptr in self._opened:
                 _lib.load().ctap_ipc_close(ctypes.c_void_p(ptr))
             self._opened = []
@@ -244,6 +247,24 @@ class SlabPropagator:
             return False
         self._flag = torch.zeros(1, dtype=torch.float32, device=self.v_local.device)
         return True
+
+    def close(self):
+        """Release the fused transport's peer mappings (collective: every rank
+        calls it).  A barrier first, so no rank unmaps a buffer another rank
+        may still be storing into; then the plan's peer tables are cleared and
+        the CUDA IPC mappings closed.  Idempotent; the NCCL transport has
+        nothing to release."""
+        if self.transport != "fused":
+            return
+        torch.cuda.synchronize(self.v_local.device)
+        dist.barrier(group=self.group)
+        self.native.clear_peer_buffers()
+        for ptr in self._opened:
+            _lib.load().ctap_ipc_close(ctypes.c_void_p(ptr))
+        self._opened = []
+        dist.barrier(group=self.group)  # every rank unmapped before the owners free
+        self.yslab = self.peer = None
+        self.transport = "closed"
 
     def _barrier(self):
         # stream-ordered: every rank's preceding pass (and its system fence)
@@ -266,6 +287,8 @@ class SlabPropagator:
         if self.layout.P == 1:
             self.native.advance(psi_local, n_steps)
             return
+        if self.transport == "closed":
+            raise RuntimeError("SlabPropagator was closed")
         if self.transport == "fused":
             addr = {"psi": psi_local.data_ptr(), "yslab": self.yslab.ptr, "peer": self.peer.ptr}
             for op in segment_schedule_fused(n_steps):

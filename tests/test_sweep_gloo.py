@@ -82,3 +82,26 @@ def test_replica_sweep_gloo(tmp_path, world):
     lines = (out / "sweep.csv").read_text().splitlines()
     assert lines[0] == "i_m,ordering,final_p_r" and len(lines) == 1 + len(seq)
     assert lines[1].split(",")[1] == "counter_intuitive" and lines[-1].split(",")[1] == "intuitive"
+
+
+class PlainCfg:
+    """Not a dataclass: run_sweep must still give each point its ordering
+    (reference runner.py:238-242 builds a config per ordering)."""
+
+    def __init__(self):
+        self.ordering = "counter_intuitive"
+
+    def sweep_values(self):
+        return np.array([0.010, 0.012])
+
+
+def test_sweep_plain_config_gets_each_ordering():
+    from paper_1309_2451_b200 import runner
+
+    cfg = PlainCfg()
+    seen = []
+    rows = runner.run_sweep(cfg, None, run_point=lambda c, i: seen.append(c.ordering) or fake_point(c, i))
+    assert seen == ["counter_intuitive", "counter_intuitive", "intuitive", "intuitive"]
+    assert [r[1] for r in rows] == seen
+    assert rows[-1][2] == fake_point(FakeCfg(ordering="intuitive"), 0.012)
+    assert cfg.ordering == "counter_intuitive"   # the caller's object is untouched
