@@ -5,13 +5,13 @@
 cfg1   64^3 run_bench harmonic trap, 1000 steps, populations every 50
 cfg2b  128x128x256 Ioffe-floor harmonic (population-moving), 5000 steps / 25
 cfg2   128x128x256 scaled-chip CTAP (configs/scaled.cfg with n_y = 128),
-       25,000 steps, PopulationRecorder every 50
+       25,000 steps, PopulationRecorder every 50 (V checked on all points)
 cfg3   256^3 paper-chip CTAP, 1000 steps / 100
-cfg4   512^3 paper-chip CTAP, 100 steps / 50 (V checked on 64^3 sampled points)
+cfg4   512^3 paper-chip CTAP, 100 steps / 50
 cfg3c64 / cfg4c64  the same in complex64 mode, gate 1e-4 against the oracle
 
-Both sides start from the identical psi0 (host-built Gaussian) and V (device
-Biot-Savart kernel, checked bit-for-bit against the oracle's C restatement).
+The cases are tests/baseline_cases.py's (shared with the driver-run
+tests/test_gpu_baseline_configs.py, which runs them at bounded step counts).
 Gates (BASELINE north_star): psi rel L2 <= 1e-10, every trace row's p_l, p_m,
 p_r within 1e-9.  The oracle is the checker only (test infrastructure).
 """
@@ -19,156 +19,24 @@ import argparse
 import json
 import os
 import sys
-import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-import numpy as np
-import torch
+import torch  # noqa: E402
 
-from oracle import potential as opot
-from oracle import split_step as orc
-from paper_1309_2451_b200 import magfield, observables, propagator, qgrid
-from paper_1309_2451_b200.constants import hbar, muB, species_mass
+import baseline_cases as bc  # noqa: E402
 
-M = species_mass("li6")
-GOLDEN = os.path.join(ROOT, "tests", "golden")
-
-
-def chip(name):
-    return dict(np.load(os.path.join(GOLDEN, f"segments_{name}.npz")))
-
-
-def run_case(name, grid, v, a0, steps, stride, half_gap, edge_threshold=None, v_check=None,
-             precision="complex128"):
-    og = orc.as_grid(grid)
-    part = observables.symmetric_partition(grid, half_gap)
-    # GPU
-    psi = qgrid.Wavefunction(a0.copy(), grid)
-    plan = propagator.make_plan(grid, v, M, 1e-6, precision=precision)
-    rec = observables.PopulationRecorder(part, stride=stride)
-    obs = [rec]
-    if edge_threshold is not None:
-        obs.append(observables.EdgeMonitor(stride=stride, threshold=edge_threshold))
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    psi, stats = propagator.evolve_real(psi, plan, steps, obs)
-    t_gpu = time.perf_counter() - t0
-    got = psi.amplitudes.astype(np.complex128)
-    del plan, psi
-    torch.cuda.empty_cache()
-    rows_gpu = rec.trace.as_array()
-    # CPU oracle
-    v_host = v.cpu().numpy() if isinstance(v, torch.Tensor) else v
-    t0 = time.perf_counter()
-    f = orc.make_factors(og, v_host, M, 1e-6)
-    t_plan = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    ref, rows = orc.evolve_with_trace(a0.copy(), og, f, steps, stride, part.xb1, part.xb2)
-    t_cpu = time.perf_counter() - t0
-    rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
-    gate_psi, gate_pop = (1e-10, 1e-9) if precision == "complex128" else (1e-4, 1e-4)
-    dpop = float(np.abs(rows_gpu[:, 1:4] - rows[:, 1:4]).max())
-    out = {
-        "case": name, "grid": list(grid.n), "steps": steps, "stride": stride,
-        "rel_l2": rel, "max_population_diff": dpop,
-        "max_norm_diff": float(np.abs(rows_gpu[:, 4] - rows[:, 4]).max()),
-        "max_edge_diff": float(np.abs(rows_gpu[:, 5] - rows[:, 5]).max()),
-        "times_equal": bool(np.array_equal(rows_gpu[:, 0], rows[:, 0])),
-        "trace_rows": int(len(rows)),
-        "final_populations_gpu": rows_gpu[-1, 1:4].tolist(),
-        "final_populations_cpu": rows[-1, 1:4].tolist(),
-        "population_range_p_l": [float(rows[:, 1].min()), float(rows[:, 1].max())],
-        "gpu_seconds": t_gpu, "gpu_steps_per_s": steps / t_gpu,
-        "cpu_seconds": t_cpu, "cpu_steps_per_s": steps / t_cpu, "cpu_plan_seconds": t_plan,
-        "cpu_threads": os.cpu_count(),
-        "precision": precision, "gates": [gate_psi, gate_pop],
-        "pass": bool(rel <= gate_psi and dpop <= gate_pop),
-    }
-    if v_check is not None:
-        out["potential_check"] = v_check
-    print(json.dumps(out), flush=True)
-    return out
-
-
-def cfg1():
-    og = orc.Grid((64, 64, 64), (20e-6, 4e-6, 1000e-6), (-10e-6, 4e-6 / 128, 0.0))
-    grid = qgrid.SimGrid(og.n, og.extents, og.origin)
-    v = orc.bench_potential(og, M, 5.0)
-    c = [og.origin[i] + og.extents[i] / 2 for i in range(3)]
-    a0 = orc.gaussian_packet(og, c, [e / 16 for e in og.extents])
-    return run_case("cfg1 64^3 harmonic", grid, v, a0, 1000, 50, 3.5e-6)
-
-
-def cfg2b():
-    og = orc.Grid((128, 128, 256), (20e-6, 4e-6, 250e-6), (-10e-6, 4e-6 / 256, 0.0))
-    grid = qgrid.SimGrid(og.n, og.extents, og.origin)
-    om = 2 * np.pi * np.array([2e3, 2e4, 20.0])
-    x, y, z = og.meshgrid()
-    v = muB / 2 * 0.03 + 0.5 * M * (om[0] ** 2 * x ** 2 + om[1] ** 2 * (y - 2e-6) ** 2
-                                    + om[2] ** 2 * (z - 125e-6) ** 2)
-    a0 = orc.gaussian_packet(og, (-4.4e-6, 2e-6, 125e-6), np.sqrt(hbar / (M * om)))
-    return run_case("cfg2b 128x128x256 Ioffe harmonic (population-moving)", grid, v, a0, 5000, 25, 3.5e-6)
-
-
-def chip_potential(grid, og, name, full_check):
-    ch = chip(name)
-    v = magfield.potential_values(magfield.ChipSegments.from_arrays(ch), grid)
-    if full_check:
-        ref = opot.potential_from_chip(ch, og.axis(0), og.axis(1), og.axis(2))
-        check = {"points": int(ref.size), "bitwise_equal": bool(np.array_equal(v.cpu().numpy(), ref))}
-    else:  # every 8th point along each axis
-        sl = [slice(3, None, 8)] * 3
-        ref = opot.potential_from_chip(ch, og.axis(0)[sl[0]], og.axis(1)[sl[1]], og.axis(2)[sl[2]])
-        got = v.cpu().numpy()[sl[0], sl[1], sl[2]]
-        check = {"points": int(ref.size), "bitwise_equal": bool(np.array_equal(got, ref)), "sampled": "every 8th"}
-    return v, check
-
-
-def cfg2():
-    og = orc.Grid((128, 128, 256), (20e-6, 4e-6, 250e-6), (-10e-6, 4e-6 / 256, 0.0))
-    grid = qgrid.SimGrid(og.n, og.extents, og.origin)
-    v, check = chip_potential(grid, og, "scaled", True)
-    a0 = orc.gaussian_packet(og, (-7e-6, 2e-6, 60e-6), (0.3e-6, 0.3e-6, 9.2e-6))
-    # the edge mass is recorded in the trace; no EdgeMonitor abort (its 5e-3
-    # threshold was tuned for the reference's ground-state psi0, not this packet)
-    return run_case("cfg2 128x128x256 scaled-chip CTAP", grid, v, a0, 25000, 50, 3.5e-6, v_check=check)
-
-
-def cfg3():
-    og = orc.Grid((256, 256, 256), (20e-6, 4e-6, 1000e-6), (-10e-6, 4e-6 / 512, 0.0))
-    grid = qgrid.SimGrid(og.n, og.extents, og.origin)
-    v, check = chip_potential(grid, og, "paper", False)
-    a0 = orc.gaussian_packet(og, (-7e-6, 1.43e-6, 200e-6), (0.25e-6, 0.12e-6, 15e-6))
-    return run_case("cfg3 256^3 paper-chip CTAP", grid, v, a0, 1000, 100, 3.5e-6, v_check=check)
-
-
-def cfg3c64():
-    og = orc.Grid((256, 256, 256), (20e-6, 4e-6, 1000e-6), (-10e-6, 4e-6 / 512, 0.0))
-    grid = qgrid.SimGrid(og.n, og.extents, og.origin)
-    v, check = chip_potential(grid, og, "paper", False)
-    a0 = orc.gaussian_packet(og, (-7e-6, 1.43e-6, 200e-6), (0.25e-6, 0.12e-6, 15e-6))
-    return run_case("cfg3 256^3 paper-chip CTAP, complex64", grid, v, a0, 1000, 100, 3.5e-6, v_check=check,
-                    precision="complex64")
-
-
-def _cfg4(precision):
-    og = orc.Grid((512, 512, 512), (20e-6, 4e-6, 1000e-6), (-10e-6, 4e-6 / 1024, 0.0))
-    grid = qgrid.SimGrid(og.n, og.extents, og.origin)
-    v, check = chip_potential(grid, og, "paper", False)
-    a0 = orc.gaussian_packet(og, (-7e-6, 1.43e-6, 200e-6), (0.25e-6, 0.12e-6, 15e-6))
-    tag = "" if precision == "complex128" else ", complex64"
-    return run_case("cfg4 512^3 paper-chip CTAP" + tag, grid, v, a0, 100, 50, 3.5e-6, v_check=check,
-                    precision=precision)
-
-
-def cfg4():
-    return _cfg4("complex128")
-
-
-def cfg4c64():
-    return _cfg4("complex64")
+CASES = {
+    "cfg1": lambda: (bc.cfg1(), 1000, "complex128"),
+    "cfg2b": lambda: (bc.cfg2b(), 5000, "complex128"),
+    "cfg2": lambda: (bc.cfg2(every=None), 25000, "complex128"),
+    "cfg3": lambda: (bc.cfg3(every=8), 1000, "complex128"),
+    "cfg4": lambda: (bc.cfg4(every=8), 100, "complex128"),
+    "cfg3c64": lambda: (bc.cfg3(every=8), 1000, "complex64"),
+    "cfg4c64": lambda: (bc.cfg4(every=8), 100, "complex64"),
+}
 
 
 def main():
@@ -179,7 +47,12 @@ def main():
     torch.cuda.set_device(0)
     results = []
     for c in args.cases:
-        results.append(globals()[c]())
+        case, steps, precision = CASES[c]()
+        r = bc.run_case(case, steps, precision=precision)
+        if precision != "complex128":
+            r["case"] += ", " + precision
+        print(json.dumps(r), flush=True)
+        results.append(r)
         os.makedirs(os.path.dirname(args.out), exist_ok=True)
         with open(args.out, "w") as fh:
             json.dump(results, fh, indent=1)

@@ -254,6 +254,28 @@ def test_zchunked_kinetic_block_bitwise(monkeypatch, precision):
     assert np.array_equal(run("32"), ref)
 
 
+@pytest.mark.parametrize("n,tables", [((1024, 16, 32), 0), ((64, 32, 64), 2), ((64, 32, 64), 3)])
+def test_zchunked_kinetic_block_other_paths(monkeypatch, n, tables):
+    """The z-chunked kinetic block also through the 1024-point x pass (4-column
+    tiles) and with the exp(-ik^2 dt/2) table (indexed at the chunk's absolute
+    z): unchanged results (both paths used to mis-address chunks)."""
+    grid = qgrid.make_grid(*n, (20e-6, 4e-6, 250e-6), origin=(-10e-6, 4e-6 / n[1] / 2, 0.0))
+    rng = np.random.default_rng(5)
+    v = 1e-30 * (1.0 + rng.random(n))
+    a0 = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+
+    def run(w):
+        monkeypatch.setenv("CTAP_ZCHUNK", w)
+        plan = propagator.make_plan(grid, v, M, 1e-6, phase_tables=tables)
+        psi = qgrid.Wavefunction(a0.copy(), grid)
+        psi, _ = propagator.evolve_real(psi, plan, 12)
+        return psi.amplitudes
+
+    ref = run("0")
+    assert np.array_equal(run("8"), ref)
+    assert np.array_equal(run("16"), ref)
+
+
 def test_complex64_has_no_systematic_rounding_drift():
     """complex64 applies no rounded constant to the data (float-float
     twiddles and sqrt(1/2), FP64 phase products): a rounded factor would
