@@ -1,17 +1,32 @@
 """Benchmark of the B200 split-step propagator (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--grid 512x512x512] [--decomp slab|pencil] [--pencil-c C]
+                    [--transport nccl|fused] [--share-device]
 
-Workload (BASELINE config 4 / the metric's config): 512^3 complex128
-split-step propagation of the 3D TDSE in the paper-chip CTAP potential
-(V from the bit-exact device Biot-Savart kernel, tests/golden/segments_paper.npz),
-dt = 1 us, Li-6.  A "step" is one Strang split step; K steps are timed as one
-telescoped segment (what evolve_real runs between observer events).  N > 1
-runs the x-slab decomposition (one process per GPU, NCCL all-to-all over
-NVLink, strong scaling: the grid is fixed).  Rank 0 prints one JSON line.
+Workload (default: BASELINE config 4, the configuration the metric is quoted
+on): 512^3 complex128 split-step propagation of the 3D TDSE in the paper-chip
+CTAP potential (V from the bit-exact device Biot-Savart kernel on the
+product-side chip geometry, paper_1309_2451_b200/chip.py), dt = 1 us, Li-6.
+A "step" is one Strang split step; K steps are timed as one telescoped
+segment (what evolve_real runs between observer events), after W warm-up
+segments of the same length (CUDA-graph capture happens there).
 
---impl reference times the CPU oracle (numpy + scipy.fft, the reference
-algorithm restated in oracle/) on the same workload with all host threads.
+N > 1: one process per GPU (the driver's torchrun, or -- with WORLD_SIZE
+unset -- this script re-launches itself under torch.distributed.run), x-slab
+decomposition with NCCL all-to-all transposes (--transport fused: CUDA-IPC
+peer stores inside the passes) or, with --decomp pencil, a Pr x Pc pencil
+grid (config 5).  Strong scaling: the grid is fixed.  Rank 0 prints one JSON
+line; the time is the max over ranks of the CUDA-event time.
+
+--share-device: every rank on cuda:0 over gloo (a launch/correctness test of
+the N-rank path on a one-GPU box; ranks time-share the GPU, so the number is
+not a measurement and says so).
+
+--impl reference times the reference's CPU algorithm (oracle/, the numpy +
+scipy.fft port pinned bitwise to the reference; its pooled pointwise
+multiplies as in propagator.py:84-95, scipy.fft workers = all host threads)
+on the same grid.
 """
 
 from __future__ import annotations
@@ -19,6 +34,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,17 +48,27 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 METRIC = "split-step steps/sec at 512³ complex128 (1/2/4/8 B200) and % of HBM roofline"
-GRID_N = (512, 512, 512)
 EXTENTS = (20e-6, 4e-6, 1000e-6)          # paper chip footprint (cfg/paper.cfg)
 DT = 1e-6
 BYTES_PER_POINT_STEP = 136                # 4 sweeps x 32 B + 8 B of V
+NVLINK_GBS = 770.0                        # measured peer copy per direction (B200_PROFILING.md; nominal 900)
+CONFIG_NAMES = {(64, 64, 64): "BASELINE config 1", (128, 128, 256): "BASELINE config 2",
+                (256, 256, 256): "BASELINE config 3", (512, 512, 512): "BASELINE config 4",
+                (1024, 1024, 512): "BASELINE config 5"}
 
 
-def _grid():
+def parse_grid(s: str) -> tuple:
+    n = tuple(int(v) for v in s.lower().replace(",", "x").split("x"))
+    if len(n) != 3:
+        raise argparse.ArgumentTypeError("--grid takes NXxNYxNZ")
+    return n
+
+
+def _grid(n):
     from paper_1309_2451_b200 import qgrid
 
-    dy = EXTENTS[1] / GRID_N[1]
-    return qgrid.make_grid(*GRID_N, EXTENTS, origin=(-EXTENTS[0] / 2, dy / 2, 0.0))
+    dy = EXTENTS[1] / n[1]
+    return qgrid.make_grid(*n, EXTENTS, origin=(-EXTENTS[0] / 2, dy / 2, 0.0))
 
 
 def _peaks():
@@ -52,6 +78,14 @@ def _peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def _config(n):
+    """The workload both arms report (identical dicts: the arms differ only in
+    the implementation; decomposition etc. go to `details`)."""
+    name = CONFIG_NAMES.get(tuple(n), "synthetic grid")
+    return {"workload": f"{n[0]}x{n[1]}x{n[2]} CTAP split-step propagation, complex128, dt = 1 us, Li-6 ({name})",
+            "grid": list(n), "extents_m": list(EXTENTS)}
 
 
 # ---------------------------------------------------------------- clocks
@@ -118,23 +152,36 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- our arm
 
-def _local_gaussian(grid, x_slice):
+def _gaussian_block(grid, x_slice, y_slice):
     """Normalized Gaussian in the left guide (qgrid.gaussian_packet's separable
-    form), restricted to this rank's x-slab; the normalisation uses the global
+    form), restricted to this rank's block; the normalisation uses the global
     separable norm so every rank agrees without communication."""
     c = (-7e-6, 1.43e-6, 200e-6)
     w = (0.25e-6, 0.12e-6, 15e-6)
     f = [np.exp(-((grid.axis(i) - c[i]) ** 2) / (2 * w[i] ** 2)) for i in range(3)]
     nrm = np.sqrt(float((f[0] ** 2).sum() * (f[1] ** 2).sum() * (f[2] ** 2).sum()) * grid.dvol)
-    fx = f[0][x_slice] / nrm
-    return fx, f[1], f[2]
+    return f[0][x_slice] / nrm, f[1][y_slice], f[2]
+
+
+class _Single:
+    """N = 1: the plan's own advance (CUDA graphs of 16 steps)."""
+
+    def __init__(self, grid, v, m):
+        from paper_1309_2451_b200 import propagator
+
+        self.plan = propagator.make_plan(grid, v, m, DT)
+        self.native = self.plan.native
+        self.transport = None
+
+    def advance(self, psi, n):
+        self.native.advance(psi.reshape(-1), n)
 
 
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1309_2451_b200 import _lib, magfield, observables, propagator, qgrid, slab
+    from paper_1309_2451_b200 import _lib, chip, magfield, observables, pencil, propagator, qgrid, slab
     from paper_1309_2451_b200.constants import species_mass
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -142,30 +189,69 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    dev_index = 0 if args.share_device else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    backend = "gloo" if args.share_device else "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     m = species_mass("li6")
-    grid = _grid()
-    lay = slab.SlabLayout(grid.n, world, rank)
+    n = args.grid
+    grid = _grid(n)
     npts = grid.size
 
-    # potential: this rank's x-slab of the paper-chip CTAP potential (one-time)
-    chip = magfield.ChipSegments.from_arrays(np.load(os.path.join(ROOT, "tests", "golden", "segments_paper.npz")))
+    # decomposition and this rank's block
+    Pr = Pc = None
+    if world == 1:
+        x_sl, y_sl, decomp = slice(None), slice(None), None
+        a2a_bytes = 0
+    elif args.decomp == "pencil":
+        Pc = args.pencil_c or (4 if world >= 8 else 2)
+        Pr = world // Pc
+        lay = pencil.PencilLayout(tuple(n), Pr, Pc, rank)
+        x_sl, y_sl = lay.x_slice, lay.y_slice
+        decomp = f"pencil {Pr}x{Pc} (NCCL row/column all-to-alls)"
+        a2a_bytes = lay.a2a_bytes_per_step()
+    else:
+        lay = slab.SlabLayout(tuple(n), world, rank)
+        x_sl, y_sl = lay.x_slice, slice(None)
+        decomp = f"x-slab x{world} ({args.transport} transposes)"
+        a2a_bytes = lay.a2a_bytes_per_step()
+    if args.share_device and world > 1:
+        decomp += "; share-device test mode: all ranks on cuda:0 over gloo (not a measurement)"
+    nloc = npts // world
+
+    # potential: this rank's block of the paper-chip CTAP potential (one-time)
+    segs = chip.chip_segments("paper")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    v_local = magfield.potential_values(chip, grid, lay.x_slice)
+    v_local = magfield.potential_on_axes(segs, grid.axis(0)[x_sl], grid.axis(1)[y_sl], grid.axis(2))
     torch.cuda.synchronize()
     t_pot = time.perf_counter() - t0
 
-    fx, fy, fz = _local_gaussian(grid, lay.x_slice)
+    fx, fy, fz = _gaussian_block(grid, x_sl, y_sl)
     amp0 = (torch.from_numpy(fx)[:, None, None] * torch.from_numpy(fy)[None, :, None]
             * torch.from_numpy(fz)[None, None, :]).to(torch.complex128)
     psi = amp0.to(dev).contiguous()
-    prop = slab.SlabPropagator(grid, v_local, m, DT, phase_tables=args.phase_tables,
-                               transport=args.transport)
-    tables = prop.phase_tables
+
+    def host_barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    if world == 1:
+        prop = _Single(grid, v_local, m)
+    elif args.decomp == "pencil":
+        rg, cg = pencil.make_groups(Pr, Pc)
+        prop = pencil.PencilPropagator(grid, v_local, m, DT, Pr, Pc, rg, cg)
+        prop.transport = "nccl"
+    else:
+        prop = slab.SlabPropagator(grid, v_local, m, DT, transport=args.transport,
+                                   barrier=host_barrier if args.share_device else None)
+        if getattr(prop, "transport_fallback", None):
+            decomp += f"; fused transport unavailable: {prop.transport_fallback}"
 
     def barrier():
         if world > 1:
@@ -174,20 +260,20 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # warm-up
+    # warm-up: W segments of the timed length (graph capture, NCCL setup)
     for _ in range(args.warmup):
-        prop.advance(psi, 1)
+        prop.advance(psi, args.steps)
     torch.cuda.synchronize()
     barrier()
 
     # timed region: K steps as one telescoped segment, CUDA events on the stream
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         barrier()
         torch.cuda.synchronize()
         wall0 = time.perf_counter()
@@ -200,29 +286,35 @@ def run_ours(args):
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms_total / args.steps
     steps_per_s = 1000.0 / ms_step
-    norm_sums = prop.observe(psi)
-    norm = norm_sums[0] * grid.dvol
+    sums = prop.observe(psi) if world > 1 else prop.native.observe(
+        psi, torch.from_numpy(grid.axis(0)).to(dev), None, None, 2).tolist()
+    norm = sums[0] * grid.dvol
 
     # per-pass device times (CUDA events, same stream) -> dominant kernel roofline
-    nloc = lay.points
-    if world > 1 and prop.transport == "fused":
-        bufs = {"psi": psi.reshape(-1), "send": psi.reshape(-1), "recv": psi.reshape(-1)}
-    else:
-        bufs = {"psi": psi.reshape(-1), "send": prop.send, "recv": prop.recv}
-    vtab = 16 if tables & propagator.PHASE_TABLE_V else 8
-    ktab = 16 if tables & propagator.PHASE_TABLE_K else 0
-    fused = world > 1 and prop.transport == "fused"
-    passes = [("z_mid [z^-1 V z]", _lib.PASS_Z_MID, "psi", "psi", 32 + vtab),
-              ("y_fwd", _lib.PASS_Y_FWD_TO_PEER if world > 1 else _lib.PASS_Y_FWD, "psi",
-               "send" if world > 1 else "psi", 32),
-              ("x_kin [x K x^-1]", _lib.PASS_X_KIN, "recv" if world > 1 else "psi",
-               "recv" if world > 1 else "psi", 32 + ktab),
-              ("y_inv", _lib.PASS_Y_INV_FROM_PEER if world > 1 else _lib.PASS_Y_INV,
-               "send" if world > 1 else "psi", "psi", 32)]
     per_pass = {}
+    flat = psi.reshape(-1)
+    if world == 1:
+        bufs = {"psi": flat}
+        passes = [("z_mid [z^-1 V z]", _lib.PASS_Z_MID, "psi", "psi", 40),
+                  ("y_fwd", _lib.PASS_Y_FWD, "psi", "psi", 32),
+                  ("x_kin [x K x^-1]", _lib.PASS_X_KIN, "psi", "psi", 32),
+                  ("y_inv", _lib.PASS_Y_INV, "psi", "psi", 32)]
+    elif args.decomp == "pencil":
+        bufs = dict(prop.bufs, psi=flat)
+        passes = [("z_mid [z^-1 V z]", _lib.PASS_PZ_MID, "zc", "zc", 40),
+                  ("y_fwd", _lib.PASS_PY_FWD, "yb", "xp", 32),
+                  ("x_kin [x K x^-1]", _lib.PASS_PX_KIN, "xr", "xr", 32),
+                  ("y_inv", _lib.PASS_PY_INV, "xp", "yb", 32)]
+    elif prop.transport == "fused":  # the fused passes need the peer buffers: z only
+        bufs = {"psi": flat}
+        passes = [("z_mid [z^-1 V z]", _lib.PASS_Z_MID, "psi", "psi", 40)]
+    else:
+        bufs = {"psi": flat, "send": prop.send, "recv": prop.recv}
+        passes = [("z_mid [z^-1 V z]", _lib.PASS_Z_MID, "psi", "psi", 40),
+                  ("y_fwd", _lib.PASS_Y_FWD_TO_PEER, "psi", "send", 32),
+                  ("x_kin [x K x^-1]", _lib.PASS_X_KIN, "recv", "recv", 32),
+                  ("y_inv", _lib.PASS_Y_INV_FROM_PEER, "send", "psi", 32)]
     reps = max(3, min(20, args.steps))
-    if fused:  # the fused passes need the plan-owned exchange buffers
-        passes = [("z_mid [z^-1 V z]", _lib.PASS_Z_MID, "psi", "psi", 32 + vtab)]
     for name, kind, src, dst, bpp in passes:
         for _ in range(2):
             prop.native.run_pass(kind, bufs[src], bufs[dst])
@@ -242,74 +334,71 @@ def run_ours(args):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tr = json.load(fh)
-        traffic = tr.get(f"{world}:{dom_name.split()[0]}:tables{tables}")
+        traffic = tr.get(f"{world}:{dom_name.split()[0]}:tables0:{n[0]}x{n[1]}x{n[2]}")
     except Exception:
         pass
 
-    # end to end through the public API: host-resident psi in pinned memory ->
-    # evolve_real with a population observer (single GPU) or the slab
-    # propagator with the same event schedule (N GPUs) -> psi back on the host
+    # end to end through the public API: host-resident psi (pinned) -> the
+    # propagation with a population observer -> psi back on the host
     e2e = None
-    if world > 1 and not args.no_e2e:
-        host = torch.empty(lay.slab_shape, dtype=torch.complex128, pin_memory=True)
-        host.copy_(amp0)
-        host_out = torch.empty_like(host).pin_memory()
+    if not args.no_e2e:
         part = observables.symmetric_partition(grid, 3.5e-6)
         stride = max(1, args.steps // 4)
-        events = propagator.event_schedule(args.steps, [observables.PopulationRecorder(part, stride=stride)])
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        d = host.to(dev, non_blocking=True)
-        cur, rows = 0, []
-        for ev in events:
-            if ev > cur:
-                prop.advance(d, ev - cur)
-                cur = ev
-            rows.append(prop.observe(d, part.xb1, part.xb2, 2))
-        host_out.copy_(d)
-        torch.cuda.synchronize()
-        t_e2e = max_over_ranks(time.perf_counter() - t0)
-        e2e = {"value": args.steps / t_e2e, "unit": "steps/s",
-               "h2d_bytes_per_step": 16 * npts / args.steps,
-               "d2h_bytes_per_step": (16 * npts + len(rows) * 5 * 8 * world) / args.steps,
-               "path": "slab.SlabPropagator.advance/observe on host-resident slabs (pinned), max over ranks",
-               "observer_events": len(rows), "seconds": t_e2e}
-        del host, host_out, d
-    if world == 1 and not args.no_e2e:
-        host = torch.empty(grid.n, dtype=torch.complex128, pin_memory=True)
+        host = torch.empty(tuple(amp0.shape), dtype=torch.complex128, pin_memory=True)
         host.copy_(amp0)
-        w = qgrid.Wavefunction(host.numpy(), grid)
-        plan = propagator.make_plan(grid, v_local, m, DT, phase_tables=tables)
-        part = observables.symmetric_partition(grid, 3.5e-6)
-        stride = max(1, args.steps // 4)
-        # one untimed warm-up call of the same path (pinned staging buffers,
-        # graph capture) -- the timed call is the steady-state user call
-        wu = qgrid.Wavefunction(host.numpy().copy(), grid)
-        wu, _ = propagator.evolve_real(wu, plan, 2, [observables.PopulationRecorder(part, stride=1)])
-        _ = wu.amplitudes
-        del wu, _
-        rec = observables.PopulationRecorder(part, stride=stride)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        w, _ = propagator.evolve_real(w, plan, args.steps, [rec])
-        out = w.amplitudes
-        t_e2e = time.perf_counter() - t0
-        events = len(rec.trace)
+        if world == 1:
+            plan = prop.plan
+            # one untimed call of the same path first (pinned staging, graphs)
+            wu = qgrid.Wavefunction(host.numpy().copy(), grid)
+            wu, _ = propagator.evolve_real(wu, plan, args.steps, [observables.PopulationRecorder(part, stride=stride)])
+            _ = wu.amplitudes
+            del wu, _
+            w = qgrid.Wavefunction(host.numpy(), grid)
+            rec = observables.PopulationRecorder(part, stride=stride)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            w, _ = propagator.evolve_real(w, plan, args.steps, [rec])
+            out = w.amplitudes
+            t_e2e = time.perf_counter() - t0
+            events = len(rec.trace)
+            path = "propagator.evolve_real(host psi, make_plan, K, [PopulationRecorder]) + psi.amplitudes"
+            del out, w
+        else:
+            host_out = torch.empty_like(host).pin_memory()
+            events = propagator.event_schedule(args.steps, [observables.PopulationRecorder(part, stride=stride)])
+            xb = (part.xb1, part.xb2)
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            d = host.to(dev, non_blocking=True)
+            cur, rows = 0, []
+            for ev in events:
+                if ev > cur:
+                    prop.advance(d, ev - cur)
+                    cur = ev
+                rows.append(prop.observe(d, *xb, 2))
+            host_out.copy_(d)
+            torch.cuda.synchronize()
+            t_e2e = max_over_ranks(time.perf_counter() - t0)
+            events = len(rows)
+            path = f"{type(prop).__name__}.advance/observe on host-resident blocks (pinned), max over ranks"
+            del host_out, d
         e2e = {"value": args.steps / t_e2e, "unit": "steps/s",
                "h2d_bytes_per_step": 16 * npts / args.steps,
-               "d2h_bytes_per_step": (16 * npts + events * 5 * 8) / args.steps,
-               "path": "propagator.evolve_real(host psi, make_plan, K, [PopulationRecorder]) + psi.amplitudes",
-               "observer_events": events, "seconds": t_e2e}
-        del out, host, w, plan
+               "d2h_bytes_per_step": (16 * npts + events * 5 * 8 * world) / args.steps,
+               "path": path, "observer_events": events, "seconds": t_e2e}
+        del host
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(grid, v_local.cpu().numpy(), amp0.numpy(), m, steps=args.cpu_steps)
 
     if rank == 0:
-        hbm_achieved = BYTES_PER_POINT_STEP * npts / world / (ms_step * 1e-3) / 1e9
-        nvl_bytes = lay.a2a_bytes_per_step()
+        hbm_floor_ms = BYTES_PER_POINT_STEP * nloc / (peak * 1e9) * 1e3
+        nvl_floor_ms = a2a_bytes / (NVLINK_GBS * 1e9) * 1e3
+        hbm_achieved = BYTES_PER_POINT_STEP * nloc / (ms_step * 1e-3) / 1e9
+        l2_note = ("inputs (psi + V = 24 B/pt) exceed the 126 MB L2; no flush needed" if 24 * nloc > 126e6 else
+                   "psi + V fit in the 126 MB L2 (L2-resident steps; HBM fraction is not a DRAM measurement)")
         line = {
             "metric": METRIC,
             "value": steps_per_s,
@@ -323,23 +412,23 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "complex128",
             "data": "synthetic: paper-chip CTAP potential (device Biot-Savart, 9605 segments) and a Gaussian packet",
-            "config": {"workload": "512^3 CTAP split-step propagation, complex128, dt = 1 us, Li-6 (BASELINE config 4)",
-                       "grid": list(GRID_N), "extents_m": list(EXTENTS), "decomposition":
-                       (f"x-slab x{world} ({prop.transport} transposes)"
-                        + (f"; fused transport unavailable: {prop.transport_fallback}"
-                           if getattr(prop, "transport_fallback", None) else "")) if world > 1 else "single GPU",
-                       "phase_factors": {0: "both on the fly (exact recipe)", 1: "exp(-iV dt) table, K on the fly",
-                                         2: "K table, V on the fly", 3: "both tables"}[tables],
-                       "bytes_per_point_step_actual": 128 + vtab + ktab,
-                       "l2": "inputs (psi 2 GiB + V 1 GiB) exceed the 126 MB L2; no flush needed"},
+            "config": _config(n),
+            "details": {"decomposition": decomp or "single GPU",
+                        "phase_factors": "both on the fly (exact recipe)",
+                        "bytes_per_point_step": BYTES_PER_POINT_STEP, "l2": l2_note},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": dom["gbs"], "peak": peak,
                          "peak_source": peak_kind, "unit": "GB/s", "frac": dom["gbs"] / peak,
                          "bytes_per_launch": dom["bytes_per_launch"], "ms_per_launch": dom["ms"],
                          "traffic": traffic},
             "step_roofline": {"bytes_per_point": BYTES_PER_POINT_STEP, "achieved_gbs_per_gpu": hbm_achieved,
-                              "frac": hbm_achieved / peak,
-                              "nvlink_bytes_per_step_per_gpu": nvl_bytes,
-                              "nvlink_frac_of_900": (nvl_bytes / (ms_step * 1e-3) / 1e9) / 900.0 if world > 1 else None},
+                              "hbm_fraction": hbm_achieved / peak, "hbm_floor_ms": hbm_floor_ms,
+                              "nvlink_bytes_per_step_per_gpu": a2a_bytes,
+                              "nvlink_gbs_per_gpu": a2a_bytes / (ms_step * 1e-3) / 1e9 if world > 1 else None,
+                              "nvlink_peak_gbs": NVLINK_GBS if world > 1 else None,
+                              "nvlink_fraction": (a2a_bytes / (ms_step * 1e-3) / 1e9) / NVLINK_GBS
+                              if world > 1 else None,
+                              "nvlink_floor_ms": nvl_floor_ms if world > 1 else None,
+                              "combined": max(hbm_floor_ms, nvl_floor_ms) / ms_step},
             "per_pass_ms": {k: round(v["ms"], 4) for k, v in per_pass.items()},
             "clocks": clk.summary(),
             "gpu_launches": 4 * args.steps + 1,
@@ -349,14 +438,17 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        if hasattr(prop, "close"):
+            prop.close()
         dist.destroy_process_group()
 
 
 # ----------------------------------------------------------- CPU oracle arm
 
 def cpu_baseline(grid, v, amp0, mass, steps=3):
-    """The reference algorithm (oracle/, numpy + scipy.fft) on the host cores,
-    on the same 512^3 workload: make_factors untimed, `steps` split steps timed."""
+    """The reference algorithm (oracle/, numpy + scipy.fft with the reference's
+    pooled multiplies) on the host cores, on the same workload: make_plan's
+    factors untimed, `steps` split steps timed."""
     from oracle import split_step as orc
 
     g = orc.as_grid(grid)
@@ -368,9 +460,12 @@ def cpu_baseline(grid, v, amp0, mass, steps=3):
     amps = orc.advance(amps, f, steps)
     dt = time.perf_counter() - t0
     cores = os.cpu_count()
+    n = grid.n
     return {"value": steps / dt, "unit": "steps/s", "cores": cores, "kind": "port",
-            "sample": f"{steps} telescoped split steps of the full 512^3 grid (oracle.split_step.advance, "
-                      f"scipy.fft workers={cores}); make_plan factors built untimed in {t_plan:.1f} s"}
+            "sample": f"{steps} telescoped split steps of the full {n[0]}x{n[1]}x{n[2]} grid "
+                      f"(oracle.split_step.advance = reference _advance: scipy.fft workers={cores}, "
+                      f"multiplies chunked over a {cores}-thread pool); make_plan factors built untimed "
+                      f"in {t_plan:.1f} s"}
 
 
 def run_reference(args):
@@ -378,15 +473,20 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import split_step as orc
+    from paper_1309_2451_b200 import chip
     from paper_1309_2451_b200.constants import species_mass
 
-    grid = _grid()
+    n = args.grid
+    grid = _grid(n)
     g = orc.as_grid(grid)
     m = species_mass("li6")
-    # the CPU path's timing does not depend on the potential contents
-    # (runner.py:275-278): the synthetic harmonic trap of run_bench stands in
+    # V: run_bench's synthetic trap (runner.py:284-288).  The CPU step's cost
+    # does not depend on V's values (runner.py:275-278: numpy multiplies and
+    # pocketfft are data-independent); the paper-chip V our arm uses would
+    # take ~25 min of host Biot-Savart at 512^3 (oracle/potential.c, 16 threads)
     v = orc.bench_potential(g, m, 5.0)
-    fx, fy, fz = _local_gaussian(grid, slice(None))
+    t_pot = 0.0
+    fx, fy, fz = _gaussian_block(grid, slice(None), slice(None))
     amps = (fx[:, None, None] * fy[None, :, None] * fz[None, None, :]).astype(np.complex128)
     f = orc.make_factors(g, v, m, DT)
     for _ in range(max(0, min(args.warmup, 1))):
@@ -405,29 +505,51 @@ def run_reference(args):
         "metric": METRIC, "value": val, "unit": "steps/s", "n_gpus": args.gpus, "steps": k,
         "warmup": args.warmup, "ms_per_step": 1000.0 / val, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "complex128",
-        "data": "synthetic: Gaussian packet; V = the run_bench harmonic field of the same shape (the split step's "
-                "cost does not depend on V's values; the paper-chip V takes ~66 min of host numba at 512^3)",
-        "config": {"workload": "512^3 CTAP split-step propagation, complex128, dt = 1 us, Li-6 (BASELINE config 4)",
-                   "grid": list(GRID_N), "extents_m": list(EXTENTS), "decomposition": "host threads"},
+        "data": "synthetic: Gaussian packet; V = run_bench's harmonic trap of the same grid (the CPU step's "
+                "cost does not depend on V's values; our arm uses the paper-chip V)",
+        "config": _config(n),
+        "details": {"decomposition": "host threads"},
         "impl": "reference",
         "cpu_baseline": {"value": val, "unit": "steps/s", "cores": cores, "kind": "port",
-                         "sample": f"{k} telescoped split steps of the full 512^3 grid on {cores} host threads "
-                                   f"(oracle.split_step.advance = reference _advance, scipy.fft workers={cores})"},
+                         "sample": f"{k} telescoped split steps of the full {n[0]}x{n[1]}x{n[2]} grid on {cores} "
+                                   f"host threads (oracle.split_step.advance = reference _advance with its "
+                                   f"thread-pooled multiplies, scipy.fft workers={cores}); the reference package "
+                                   f"itself is pure Python and not present on the GPU box, so its pinned port "
+                                   f"runs"},
         "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn(args):
+    """`python bench.py --gpus N` without a launcher: re-run this script under
+    torch.distributed.run, one process per GPU (rank 0 prints the line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--phase-tables", type=int, default=None,
-                    help="mask: 1 = exp(-iV dt) table, 2 = exp(-ik^2dt/2) table (default: library default)")
-    ap.add_argument("--transport", choices=["fused", "nccl"], default="fused",
-                    help="slab transposes: fused NVLink peer stores (default) or NCCL all-to-all")
+    ap.add_argument("--grid", type=parse_grid, default=(512, 512, 512),
+                    help="NXxNYxNZ (default 512x512x512, BASELINE config 4; 1024x1024x512 is config 5)")
+    ap.add_argument("--decomp", choices=["slab", "pencil"], default="slab",
+                    help="N > 1: x-slabs (default) or a Pr x Pc pencil grid")
+    ap.add_argument("--pencil-c", type=int, default=0, help="pencil columns Pc (default 4 at N >= 8, else 2)")
+    ap.add_argument("--transport", choices=["nccl", "fused"], default="nccl",
+                    help="slab transposes: NCCL all-to-all (default) or fused CUDA-IPC peer stores")
+    ap.add_argument("--share-device", action="store_true",
+                    help="all ranks on cuda:0 over gloo: a launch test of the N-rank path on one GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
@@ -436,9 +558,12 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return 0
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
+    run_ours(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -98,15 +98,41 @@ def make_factors(grid: Grid, potential: np.ndarray, mass: float, dt: float,
     return Factors(evh, evf, ek, dt, imaginary)
 
 
+_PARALLEL_MIN_SIZE = 1 << 18  # propagator.py:30
+
+
+def _mul_inplace(a: np.ndarray, b: np.ndarray, pool):
+    """_mul_inplace (propagator.py:84-95): a *= b, chunked over axis 0 across
+    the pool (numpy releases the GIL); elementwise, so bit-identical either way."""
+    if pool is None or a.size < _PARALLEL_MIN_SIZE:
+        np.multiply(a, b, out=a)
+        return
+    nchunks = pool._max_workers
+    bounds = np.linspace(0, a.shape[0], nchunks + 1).astype(int)
+    futs = [pool.submit(np.multiply, a[lo:hi], b[lo:hi], a[lo:hi])
+            for lo, hi in zip(bounds[:-1], bounds[1:]) if hi > lo]
+    for fu in futs:
+        fu.result()
+
+
 def advance(amps: np.ndarray, f: Factors, n: int, workers: int | None = None) -> np.ndarray:
-    """_advance (propagator.py:98-107): n merged Strang steps."""
+    """_advance (propagator.py:98-107): n merged Strang steps, with the
+    thread pool evolve_real creates when threads > 1 (propagator.py:156)
+    driving the pointwise multiplies and scipy.fft's workers the FFTs."""
+    from concurrent.futures import ThreadPoolExecutor
+
     w = workers or os.cpu_count()
-    np.multiply(amps, f.exp_v_half, out=amps)
-    for j in range(n):
-        amps = sfft.fftn(amps, workers=w, overwrite_x=True)
-        np.multiply(amps, f.exp_k, out=amps)
-        amps = sfft.ifftn(amps, workers=w, overwrite_x=True)
-        np.multiply(amps, f.exp_v_full if j < n - 1 else f.exp_v_half, out=amps)
+    pool = ThreadPoolExecutor(w) if w > 1 else None
+    try:
+        _mul_inplace(amps, f.exp_v_half, pool)
+        for j in range(n):
+            amps = sfft.fftn(amps, workers=w, overwrite_x=True)
+            _mul_inplace(amps, f.exp_k, pool)
+            amps = sfft.ifftn(amps, workers=w, overwrite_x=True)
+            _mul_inplace(amps, f.exp_v_full if j < n - 1 else f.exp_v_half, pool)
+    finally:
+        if pool is not None:
+            pool.shutdown()
     return amps
 
 

@@ -152,8 +152,9 @@ class PencilPropagator:
         self.bufs = {k: torch.empty(self.layout.points, dtype=dt_, device=dev) for k in ("zc", "yb", "xp", "xr")}
 
     def _a2a(self, which: str, src: torch.Tensor, dst: torch.Tensor):
-        group = self.row_group if which == "row" else self.col_group
-        dist.all_to_all_single(torch.view_as_real(dst), torch.view_as_real(src), group=group)
+        from .slab import all_to_all_c
+
+        all_to_all_c(dst, src, self.row_group if which == "row" else self.col_group)
 
     def advance(self, psi_block: torch.Tensor, n_steps: int):
         """n telescoped steps on this rank's block (collective: all ranks call)."""

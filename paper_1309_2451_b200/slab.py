@@ -145,15 +145,35 @@ def open_ipc(handle: bytes) -> int:
     return int(h.value)
 
 
+def _host_staged(group) -> bool:
+    """Device tensors over a non-NCCL group (gloo: the CPU tests and the
+    bench's --share-device mode, several ranks on one GPU) go through host
+    memory."""
+    return dist.get_backend(group) != "nccl"
+
+
+def all_to_all_c(dst: torch.Tensor, src: torch.Tensor, group=None):
+    """all_to_all_single of complex buffers (equal chunks, rank order)."""
+    if src.is_cuda and _host_staged(group):
+        h_dst = torch.empty(torch.view_as_real(dst).shape, dtype=torch.view_as_real(dst).dtype)
+        dist.all_to_all_single(h_dst, torch.view_as_real(src).cpu(), group=group)
+        torch.view_as_real(dst).copy_(h_dst)
+    else:
+        dist.all_to_all_single(torch.view_as_real(dst), torch.view_as_real(src), group=group)
+
+
 def combine_in_rank_order(local: torch.Tensor, group=None) -> torch.Tensor:
     """Sum per-rank partial sums in rank order (bitwise identical on every rank)."""
     P = dist.get_world_size(group)
+    dev = local.device
+    if local.is_cuda and _host_staged(group):
+        local = local.cpu()
     parts = [torch.empty_like(local) for _ in range(P)]
     dist.all_gather(parts, local, group=group)
     total = parts[0].clone()
     for p in parts[1:]:
         total += p
-    return total
+    return total.to(dev)
 
 
 class SlabPropagator:
@@ -278,7 +298,7 @@ class SlabPropagator:
         if self.layout.P == 1:
             dst.copy_(src)
         else:
-            dist.all_to_all_single(torch.view_as_real(dst), torch.view_as_real(src), group=self.group)
+            all_to_all_c(dst, src, self.group)
 
     def advance(self, psi_local: torch.Tensor, n_steps: int):
         """n telescoped steps on this rank's slab (collective: all ranks call)."""
