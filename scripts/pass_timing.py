@@ -22,8 +22,12 @@ def main():
     m = species_mass("li6")
     grid = qgrid.make_grid(nx, ny, nz, (20e-6, 4e-6, 1000e-6), origin=(-10e-6, 4e-6 / ny / 2, 0.0))
     n = nx * ny * nz
-    v = torch.full((nx, ny, nz), muB / 2 * 0.03, dtype=torch.float64, device="cuda")
-    v += torch.rand_like(v) * 1e-29
+    # Ioffe floor + anisotropic harmonic trap: point-to-point varying phases
+    # like the CTAP potential's (a flat V makes every sincos gather hit one line)
+    x, y, z = (torch.as_tensor(a, device="cuda") for a in grid.meshgrid())
+    om = 2 * np.pi * np.array([2e3, 2e4, 20.0])
+    v = muB / 2 * 0.03 + 0.5 * m * (om[0] ** 2 * x ** 2 + om[1] ** 2 * (y - 2e-6) ** 2 + om[2] ** 2 * (z - 5e-4) ** 2)
+    del x, y, z
     prec = os.environ.get('CTAP_PRECISION', 'complex128')
     plan = propagator.make_plan(grid, v, m, 1e-6, phase_tables=int(os.environ.get('CTAP_PHASE_TABLES', '0')), precision=prec)
     psi = (torch.randn(nx, ny, nz, dtype=propagator.PRECISIONS[prec], device="cuda") * 1e-3).contiguous()

@@ -72,6 +72,8 @@ def test_plan_create_validation(kw, code, msg):
 def test_null_arguments_rejected():
     lib = _lib.load()
     assert lib.ctap_advance(None, None, 1, None) == _lib.CTAP_EINVAL
+    assert lib.ctap_advance_observe(None, None, 1, None, None, None, 2, None, None) == _lib.CTAP_EINVAL
+    assert lib.ctap_set_peer_buffers(None, 0, None, 0) == _lib.CTAP_EINVAL
     assert lib.ctap_observe(None, None, None, None, None, 2, None, None) == _lib.CTAP_EINVAL
     assert lib.ctap_potential(None, 1, None, 1, None, 1, None, None, None, 0,
                               0., 0., 0., 0., 0., 0., 0., 0., None, None) == _lib.CTAP_EINVAL
