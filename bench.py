@@ -327,6 +327,41 @@ def run_ours(args):
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / reps
         per_pass[name] = {"ms": ms, "bytes_per_launch": bpp * nloc, "gbs": bpp * nloc / (ms * 1e-3) / 1e9}
+    # cost of an observer event (PopulationRecorder sums) on top of a K-step
+    # segment: fused into the segment-end pass vs the standalone reduction
+    obs_cost = None
+    if world == 1:
+        part = observables.symmetric_partition(grid, 3.5e-6)
+        xs_d = torch.from_numpy(grid.axis(0)).to(dev)
+        xb = (torch.from_numpy(part.xb1).to(dev), torch.from_numpy(part.xb2).to(dev))
+
+        def timed(fn, reps=5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(reps):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+
+        # one-step segments (short enough that clock drift does not swamp the
+        # difference), the three variants interleaved, median of 7 rounds
+        plain = lambda: prop.native.advance(flat, 1)
+        fusedo = lambda: prop.native.advance_observe(flat, 1, xs_d, *xb, 2)
+        separate = lambda: (prop.native.advance(flat, 1), prop.native.observe(flat, xs_d, *xb, 2))
+        for f in (plain, fusedo, separate):
+            f()
+        d_f, d_s, t_p = [], [], []
+        for _ in range(7):
+            tp, tf, ts = timed(plain), timed(fusedo), timed(separate)
+            t_p.append(tp)
+            d_f.append(tf - tp)
+            d_s.append(ts - tp)
+        obs_cost = {"segment_steps": 1, "segment_ms": statistics.median(t_p),
+                    "extra_ms_fused": statistics.median(d_f),
+                    "extra_ms_standalone_reduction": statistics.median(d_s),
+                    "method": "CUDA events, 1-step segments x 5, the variants interleaved, median of 7"}
     dom_name = max(per_pass, key=lambda k: per_pass[k]["ms"])
     dom = per_pass[dom_name]
     peak, peak_kind = _peaks()
@@ -430,6 +465,7 @@ def run_ours(args):
                               "nvlink_floor_ms": nvl_floor_ms if world > 1 else None,
                               "combined": max(hbm_floor_ms, nvl_floor_ms) / ms_step},
             "per_pass_ms": {k: round(v["ms"], 4) for k, v in per_pass.items()},
+            "observer_event": obs_cost,
             "clocks": clk.summary(),
             "gpu_launches": 4 * args.steps + 1,
             "e2e": e2e,

@@ -140,6 +140,17 @@ CTAP_API int ctap_plan_destroy(ctap_plan* plan);
  * n_steps == 0 leaves psi untouched. */
 CTAP_API int ctap_advance(ctap_plan* plan, void* psi_dev, int64_t n_steps, void* stream);
 
+/* evolve_real's segment + observer event (propagator.py:160-168): n telescoped
+ * steps, then the raw sums of ctap_observe ([sum rho, left, middle, right,
+ * edge(margin)] into out_dev[5]) -- computed inside the segment-end pass
+ * [z^-1 . Vh] from the registers it writes psi from (block partials, summed
+ * in a fixed order), so the event reads no extra byte of psi.  n == 0 (or an
+ * imaginary-time plan) runs the standalone ctap_observe.  xs/xb1/xb2 as for
+ * ctap_observe (device pointers; xb1 = xb2 = NULL: no partition). */
+CTAP_API int ctap_advance_observe(ctap_plan* plan, void* psi_dev, int64_t n_steps, const double* xs,
+                                  const double* xb1, const double* xb2, int32_t margin, double* out_dev,
+                                  void* stream);
+
 /* One axis pass (the building block of ctap_advance, exposed for the slab
  * decomposition and the plain 3D FFT of kinetic_expectation). z passes are in
  * place (in == out).  Y/X passes may be in place in the natural layout. */

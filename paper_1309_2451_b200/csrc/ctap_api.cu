@@ -257,6 +257,7 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
   cudaFree(p->twiddles);
   cudaFree(p->twiddles32);
   cudaFree(p->sctab);
+  cudaFree(p->obs_partial);
   cudaFree(p->red_partial);
   cudaFree(p->vi_dev);
   cudaFree(p->expv_dev);
@@ -386,8 +387,40 @@ CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
     } else {
       CUDA_TRY(kin_block(p, psi, st), "ctap_advance");
     }
-    CUDA_TRY(ctap_run_pass(p, j < n - 1 ? CTAP_PASS_Z_MID : CTAP_PASS_Z_LAST, psi, psi, st), "ctap_advance");
+    if (j < n - 1 || !p->skip_last)
+      CUDA_TRY(ctap_run_pass(p, j < n - 1 ? CTAP_PASS_Z_MID : CTAP_PASS_Z_LAST, psi, psi, st), "ctap_advance");
   }
+  return CTAP_OK;
+}
+
+// ctap_advance followed by an observer event, the event's sums fused into the
+// segment-end pass (evolve_real's advance + PopulationRecorder/EdgeMonitor,
+// propagator.py:160-168, observables.py:74-110).
+CTAP_API int ctap_advance_observe(ctap_plan* p, void* psi, int64_t n, const double* xs, const double* xb1,
+                                  const double* xb2, int32_t margin, double* out, void* stream) {
+  if (!p || !psi || !out || !xs) return fail(CTAP_EINVAL, "null argument");
+  if ((xb1 == nullptr) != (xb2 == nullptr)) return fail(CTAP_EINVAL, "xb1 and xb2 must both be given");
+  if (margin < 1) return fail(CTAP_EINVAL, "margin_cells must be >= 1");
+  if (n < 0) return fail(CTAP_EINVAL, "n_steps must be >= 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0 || p->slab_p != 1 || p->kbuf || p->mode != 0) {
+    // nothing to fuse into (or a plan whose segment end is not the plain z
+    // pass): the step(s), then the standalone reduction
+    const int rc = ctap_advance(p, psi, n, stream);
+    if (rc != CTAP_OK) return rc;
+    CUDA_TRY(ctap_run_observe(p, psi, xs, xb1, xb2, margin, out, st), "ctap_advance_observe");
+    return CTAP_OK;
+  }
+  if (!p->obs_partial)
+    CUDA_TRY(cudaMalloc((void**)&p->obs_partial, sizeof(double) * 5 * ctap_z_blocks(p)), "ctap_advance_observe");
+  // all but the last pass of the segment: ctap_advance of n steps minus its
+  // final [z^-1 . Vh] (the same launches, graphs included)
+  p->skip_last = 1;
+  const int rc = ctap_advance(p, psi, n, stream);
+  p->skip_last = 0;
+  if (rc != CTAP_OK) return rc;
+  CUDA_TRY(ctap_run_z_last_observe(p, psi, xs, xb1, xb2, margin, p->obs_partial, st), "ctap_advance_observe");
+  CUDA_TRY(ctap_run_finalize5(p->obs_partial, ctap_z_blocks(p), out, st), "ctap_advance_observe");
   return CTAP_OK;
 }
 

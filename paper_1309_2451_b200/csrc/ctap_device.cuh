@@ -222,6 +222,17 @@ struct SyncNamed {  // T threads (a multiple of 32) of one line: named barrier
   }
 };
 
+// Table loads: read-only global through the L1 (default), or plain loads of a
+// CTA's shared-memory copy.  (Staging the 512-point twiddles and the kinetic
+// sincos table in the ring x pass's shared memory measured slower: 1.14 ->
+// 1.31-1.36 ms, the staged loads raise register pressure to spills; r02.)
+struct LdgLoad {
+  __device__ __forceinline__ static double2 ld(const double2* p) { return __ldg(p); }
+};
+struct SmemLoad {  // the pointer must derive from the kernel's shared array (LDS after inlining)
+  __device__ __forceinline__ static double2 ld(const double2* p) { return *p; }
+};
+
 // Twiddles of a complex128 radix-8 butterfly: u[r] *= w^r (w = exp(-2 pi i
 // k / (8 NS)), conjugated for DIR > 0).  Three table loads (w, w^2, w^4; the
 // table's column k at stride NS) and the other four as their products: the
@@ -230,9 +241,9 @@ struct SyncNamed {  // T threads (a multiple of 32) of one line: named barrier
 // products carry ~1 ulp more rounding than table values; FFT roundoff is not
 // what the 1e-10 parity gate is sensitive to.  Every radix-8
 // kernel uses this helper, so all of them stay bitwise interchangeable.
-template <int DIR>
+template <int DIR, typename LD = LdgLoad>
 __device__ __forceinline__ void radix8_twiddles(double2* u, const double2* __restrict__ col, int NS) {
-  const double2 w1 = __ldg(col), w2 = __ldg(col + NS), w4 = __ldg(col + 3 * NS);
+  const double2 w1 = LD::ld(col), w2 = LD::ld(col + NS), w4 = LD::ld(col + 3 * NS);
   const double2 w3 = cmul(w1, w2);
   u[1] = tw_mul<DIR>(u[1], w1);
   u[2] = tw_mul<DIR>(u[2], w2);
@@ -367,10 +378,9 @@ __constant__ double kSC[16] = {
 
 // the out-of-range path of fast_sincos, kept out of line: inlined at every
 // point of a kernel it would multiply the code size
-__device__ __noinline__ inline void slow_sincos(double phi, const double2* __restrict__ tab, double* s, double* c) {
+__device__ __noinline__ inline void slow_sincos(double phi, double f, double* s, double* c) {
   double ss, cc;
   sincos(phi, &ss, &cc);
-  const double f = __ldg(&tab[0].x);
   *s = ss * f;
   *c = cc * f;
 }
@@ -391,6 +401,7 @@ __device__ __noinline__ inline void slow_sincos(double phi, const double2* __res
 // |phi| >= 2^20 falls back to the library (never on CTAP grids, where
 // |phi| < 1e6) and applies f = tab[0].x explicitly.  Errors of an ulp in the
 // factor are harmless (only the phase must be bit-exact).
+template <typename LD = LdgLoad>
 __device__ __forceinline__ void fast_sincos(double phi, const double2* __restrict__ tab, double* s, double* c) {
   if (fabs(phi) < 1048576.0) {
     const double t = fma(phi, kSC[0], kSC[4]);
@@ -418,11 +429,11 @@ __device__ __forceinline__ void fast_sincos(double phi, const double2* __restric
     }
     const double sr = fma(r * r2, ps, r);
     const double cr = fma(r2, pc, 1.0);
-    const double2 tb = __ldg(&tab[n & (kSCN - 1)]);
+    const double2 tb = LD::ld(&tab[n & (kSCN - 1)]);
     *c = fma(tb.x, cr, -(tb.y * sr));
     *s = fma(tb.y, cr, tb.x * sr);
   } else {
-    slow_sincos(phi, tab, s, c);
+    slow_sincos(phi, LD::ld(tab).x, s, c);
   }
 }
 

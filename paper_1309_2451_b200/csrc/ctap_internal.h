@@ -82,6 +82,8 @@ struct ctap_plan {
   void* peer_y[16];        // fused slab transposes: every rank's y-slab buffer
   void* peer_p[16];        // and peer-major buffer (peer-mapped device addresses)
   double* red_partial;     // reduction scratch
+  double* obs_partial;     // per-block partials of the fused segment-end observer sums (lazy)
+  int skip_last;           // ctap_advance_observe: ctap_advance stops before the segment-end pass
   // CUDA graph of M interior steps (launch-bound small grids), captured on a
   // private stream for one psi pointer and replayed on the caller's stream
   cudaStream_t cap_stream;
@@ -102,6 +104,10 @@ void ctap_append_twiddles2(std::vector<double>& t, int off2[5]);
 namespace ctap {
 struct ZArgs;
 }
+int64_t ctap_z_blocks(const ctap_plan* p);
+cudaError_t ctap_run_z_last_observe(const ctap_plan* p, void* psi, const double* xs, const double* xb1,
+                                    const double* xb2, int margin, double* partial, cudaStream_t st);
+cudaError_t ctap_run_finalize5(const double* partial, int64_t nblocks, double* out, cudaStream_t st);
 cudaError_t ctap_run_z2(const ctap_plan* p, int tkind, bool vtab, int ch, const ctap::ZArgs& a, cudaStream_t st);
 static inline int ilog2i(int64_t v) {
   int l = 0;

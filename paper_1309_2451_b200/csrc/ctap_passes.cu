@@ -46,6 +46,10 @@
 #ifndef CTAP_Z_MINB
 #define CTAP_Z_MINB 3
 #endif
+// threads per z-pass block (lines per block = this / (L/8))
+#ifndef CTAP_Z_THREADS
+#define CTAP_Z_THREADS 256
+#endif
 #ifndef CTAP_Z_MINB_TAB
 #define CTAP_Z_MINB_TAB 2
 #endif
@@ -62,7 +66,7 @@ namespace ctap {
 template <int L, typename CV>
 struct ZCfg {
   static constexpr int T = L / kElems;
-  static constexpr int C = (256 / T) > 0 ? (256 / T) : 1;  // lines per block
+  static constexpr int C = (CTAP_Z_THREADS / T) > 0 ? (CTAP_Z_THREADS / T) : 1;  // lines per block
   static constexpr int threads = C * T;
   static constexpr int smem_line = L + L / 8;             // padded complex per line
   static constexpr size_t smem = (size_t)C * smem_line * sizeof(CV);
@@ -118,7 +122,54 @@ struct ZMinBlocks {
   static constexpr int value = (KIND == T_VMID && VTAB) ? CTAP_Z_MINB_TAB : CTAP_Z_MINB;
 };
 
-template <int L, int KIND, bool VTAB, typename CV, int CH = 0>
+// The five observer sums of this thread's points (psi after the segment-end
+// pass, in registers), reduced over the block in a fixed order and stored as
+// the block's partial: the reduction of observables.py:74-110 fused into the
+// write-back of the last pass, so an observer event reads no extra byte of
+// psi.  Deterministic: fixed per-thread order, shuffle tree,
+// warp order; the finalize sums the block partials in a fixed order.
+template <int L, typename CV>
+__device__ __forceinline__ void z_observe(const ZArgs& a, const CV* v, int t, uint32_t line, bool active) {
+  constexpr int T = L / kElems;
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (active) {
+    const uint32_t x = line / a.ny, y = line - x * a.ny;
+    const int mg = a.margin;
+    const bool line_edge = (int)x < mg || (int)x >= (int)a.nx - mg || (int)y < mg || (int)y >= (int)a.ny - mg;
+    const double xv = __ldg(&a.xs[x]);
+#pragma unroll
+    for (int m = 0; m < kElems; ++m) {
+      const int z = t + m * T;
+      const double rho = (double)v[m].x * v[m].x + (double)v[m].y * v[m].y;
+      acc[0] += rho;
+      if (a.xb1 != nullptr) {
+        const bool in_l = xv < __ldg(&a.xb1[z]);
+        const bool in_r = xv >= __ldg(&a.xb2[z]);
+        if (in_l) acc[1] += rho;
+        if (in_r) acc[3] += rho;
+        if (!(in_l || in_r)) acc[2] += rho;
+      }
+      if (line_edge || z < mg || z >= L - mg) acc[4] += rho;
+    }
+  }
+  __shared__ double sh[5][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    double s = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sh[k][warp] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[threadIdx.x][w];
+    a.obs_partial[(size_t)blockIdx.x * 5 + threadIdx.x] = s;
+  }
+}
+
+template <int L, int KIND, bool VTAB, typename CV, int CH = 0, bool OBS = false>
 __global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::value) zline_kernel(ZArgs a, const TwOf<CV>* __restrict__ tw) {
   using Cfg = ZCfg<L, CV>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -147,6 +198,7 @@ __global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::
 #pragma unroll
     for (int m = 0; m < kElems; ++m) __stcg(&psi[at_out(t + m * Cfg::T)], v[m]);
   }
+  if constexpr (OBS) z_observe<L>(a, v, t, line, active);
 }
 
 // ---------------------------------------------------------------------------
@@ -223,10 +275,10 @@ __global__ void __launch_bounds__(TileCfg<L, CV, W>::threads,
 // ---------------------------------------------------------------------------
 
 
-template <int L, int KIND, bool VTAB, typename CV, int CH = 0>
+template <int L, int KIND, bool VTAB, typename CV, int CH = 0, bool OBS = false>
 static cudaError_t launch_z(const ZArgs& a, const TwOf<CV>* tw, cudaStream_t st) {
   using Cfg = ZCfg<L, CV>;
-  auto k = zline_kernel<L, KIND, VTAB, CV, CH>;
+  auto k = zline_kernel<L, KIND, VTAB, CV, CH, OBS>;
   static std::atomic<uint64_t> attr_done{0};
   if (cudaError_t e = ctap_smem_attr(k, Cfg::smem, attr_done)) return e;
   k<<<(a.nlines + Cfg::C - 1) / Cfg::C, Cfg::threads, Cfg::smem, st>>>(a, tw);
@@ -422,6 +474,49 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
 
 cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* out, cudaStream_t st) {
   return ctap_run_pass_z(p, kind, in, out, 0, p->n[2], st);
+}
+
+// number of blocks (= partials) of the segment-end z pass
+int64_t ctap_z_blocks(const ctap_plan* p) {
+  const int64_t nlines = p->nx_local * p->n[1];
+  const int T = (int)(p->n[2] / kElems);
+  const int C = (CTAP_Z_THREADS / T) > 0 ? (CTAP_Z_THREADS / T) : 1;
+  return (nlines + C - 1) / C;
+}
+
+// [z^-1 . Vh] with the observer sums fused (single-GPU plans): block partials
+// of [sum rho, left, middle, right, edge(margin)] into `partial`
+// (ctap_z_blocks(p) x 5 doubles)
+cudaError_t ctap_run_z_last_observe(const ctap_plan* p, void* psi, const double* xs, const double* xb1,
+                                    const double* xb2, int margin, double* partial, cudaStream_t st) {
+  const int64_t nz = p->n[2];
+  ZArgs a{};
+  a.psi = psi;
+  a.out = psi;
+  a.lzc = 0;
+  a.cs = 0;
+  a.nlines = (uint32_t)(p->nx_local * p->n[1]);
+  a.xs = xs;
+  a.xb1 = xb1;
+  a.xb2 = xb2;
+  a.obs_partial = partial;
+  a.ny = (uint32_t)p->n[1];
+  a.nx = (uint32_t)p->n[0];
+  a.margin = margin;
+  PhaseArgs& ph = a.ph;
+  ph.vi = p->vi_dev;
+  ph.expv = p->expv_dev;
+  ph.dt_i = p->dt_i;
+  ph.imag = p->mode == 1;
+  ph.sct = p->sctab;
+  ph.sctk = p->sctab + kSCN;
+  const Tw tw = twid(p, nz);
+  const bool c64 = p->dtype == CTAP_C64;
+#define CTAP_ZO(LL)                                                                        \
+  (c64 ? launch_z<LL, T_VLAST, false, float2, 0, true>(a, tw.f, st)                         \
+       : launch_z<LL, T_VLAST, false, double2, 0, true>(a, tw.d, st))
+  CTAP_BY_LENGTH(nz, CTAP_ZO)
+#undef CTAP_ZO
 }
 
 // A strided pass restricted to the z columns [z0, z0 + zn) (zn a multiple of

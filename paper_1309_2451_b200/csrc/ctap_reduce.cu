@@ -65,13 +65,13 @@ struct ObserveF {
   const double* xb2;
   int64_t nyz, ny, nz, nx_global, x_off, ny_global, y_off;
   int margin;
+  int lyz, lz;  // log2(ny nz), log2(nz): every extent is a power of two (shifts, not divisions)
   __device__ __forceinline__ void operator()(int64_t i, double (&acc)[5]) const {
     const CV a = psi[i];
     const double rho = (double)a.x * a.x + (double)a.y * a.y;
-    int64_t x = i / nyz;
-    int64_t r = i - x * nyz;
-    int64_t y = r / nz;
-    int64_t z = r - y * nz;
+    const int64_t x = i >> lyz;
+    const int64_t y = (i >> lz) & (ny - 1);
+    const int64_t z = i & (nz - 1);
     acc[0] += rho;
     if (xb1 != nullptr) {
       double xv = xs[x];
@@ -96,13 +96,13 @@ struct K2F {
   const double* ky2;
   const double* kz2;
   int64_t nylz, nyl, nz, y_off;
+  int lylz, lz;  // log2(nyl nz), log2(nz)
   __device__ __forceinline__ void operator()(int64_t i, double (&acc)[2]) const {
     const CV a = phi[i];
     const double rho = (double)a.x * a.x + (double)a.y * a.y;
-    int64_t x = i / nylz;
-    int64_t r = i - x * nylz;
-    int64_t y = r / nz;
-    int64_t z = r - y * nz;
+    const int64_t x = i >> lylz;
+    const int64_t y = (i >> lz) & (nyl - 1);
+    const int64_t z = i & (nz - 1);
     double k2 = (kx2[x] + ky2[y + y_off]) + kz2[z];
     acc[0] += k2 * rho;
     acc[1] += rho;
@@ -182,6 +182,8 @@ static cudaError_t observe_t(const ctap_plan* p, const void* psi, const double* 
   f.x_off = (int64_t)(p->pen_c ? p->pen_a : p->slab_r) * p->nx_local;
   f.y_off = p->pen_c ? (int64_t)p->pen_b * p->ny_pos : 0;
   f.margin = margin;
+  f.lyz = ilog2i(f.nyz);
+  f.lz = ilog2i(f.nz);
   return run_reduce<5>(p, f, p->nx_local * f.nyz, out, st);
 }
 
@@ -202,7 +204,15 @@ static cudaError_t k2_t(const ctap_plan* p, const void* phi, double* out, cudaSt
   f.nz = p->n[2];
   f.nylz = f.nyl * f.nz;
   f.y_off = (int64_t)p->slab_r * f.nyl;
+  f.lylz = ilog2i(f.nylz);
+  f.lz = ilog2i(f.nz);
   return run_reduce<2>(p, f, p->n[0] * f.nylz, out, st);
+}
+
+// fixed-order sum of the fused z pass's block partials (ctap_advance_observe)
+cudaError_t ctap_run_finalize5(const double* partial, int64_t nblocks, double* out, cudaStream_t st) {
+  finalize_kernel<5><<<1, kRedThreads, 0, st>>>(partial, (int)nblocks, out);
+  return cudaGetLastError();
 }
 
 cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, cudaStream_t st) {

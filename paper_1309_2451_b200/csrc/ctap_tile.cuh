@@ -40,6 +40,14 @@ struct ZArgs {
   // at (z >> lzc) cs + l 2^lzc + (z & (2^lzc - 1)), cs = nlines 2^lzc
   void* out;
   uint32_t lzc, cs;
+  // fused observer sums of the segment-end pass [z^-1 . Vh] (single GPU):
+  // per block [sum rho, left, middle, right, edge] into obs_partial[5 block]
+  const double* xs;    // x axis (m)
+  const double* xb1;   // guide boundaries per z (null: no partition)
+  const double* xb2;
+  double* obs_partial;
+  uint32_t ny, nx;     // line = x ny + y
+  int margin;
 };
 
 // squared angular wavenumber of FFT index i on an axis of n points with

@@ -34,6 +34,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "ctap_device.cuh"
 #include "ctap_internal.h"
@@ -50,6 +51,8 @@ constexpr int kGroups = CTAP_WL_GROUPS;  // ring: tiles in computation at once
 constexpr int kBufs = 3;    // ring: tile buffers
 constexpr int kRingThreads = kGroups * kCols * 32;  // 2 groups: 16 warps, 4 per SM sub-partition, 128 registers each
 constexpr int kTileThreads = kCols * 32;
+// full/done mbarriers + fill counters of the ring, padded to 16 bytes
+constexpr size_t kRingBarBytes = ((2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t)) + 15) / 16 * 16;
 #ifndef CTAP_FFT512
 #define CTAP_FFT512 1
 #endif
@@ -114,12 +117,17 @@ using SwzCol = SwzColT<8>;
 
 // exp(-i k^2 dt/2)/N (real time: (cos, sin); imaginary time: (decay, 0)),
 // the recipe of mul_kphase (ctap_tile.cuh)
-__device__ __forceinline__ double2 kfactor(double kx2, double ky2, double kz2, const PhaseArgs& a) {
+template <typename LD = LdgLoad>
+__device__ __forceinline__ double2 kfactor(double kx2, double ky2, double kz2, const PhaseArgs& a,
+                                           const double2* sctk) {
   const double phi = k_phase(kx2, ky2, kz2, a.len2, a.dt_i);
   if (a.imag) return make_double2(exp(phi) * a.scale, 0.0);
   double s, c;
-  fast_sincos(phi, a.sctk, &s, &c);
+  fast_sincos<LD>(phi, sctk, &s, &c);
   return make_double2(c, s);
+}
+__device__ __forceinline__ double2 kfactor(double kx2, double ky2, double kz2, const PhaseArgs& a) {
+  return kfactor<LdgLoad>(kx2, ky2, kz2, a, a.sctk);
 }
 __device__ __forceinline__ void apply_k(double2& v, double2 f, int imag) {
   if (imag) dscale(v, f.x);
@@ -141,7 +149,7 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src) {
 //   stage-1 scatter (NS = 8): 512 (j >> 3) + 64 r + T(r)
 //   gathers of e = lane + 32 m: 256 m + R(m & 1), R(p) = 8 S + (c ^ (S & 7)),
 //                               S = lane ^ ((lane >> 3) + 4 p)
-template <int DIR>
+template <int DIR, typename LD = LdgLoad>
 __device__ __forceinline__ void fft512_warp(double2 (&v)[16], int lane, int c, const double2* __restrict__ tw,
                                             double2* buf) {
   using P = Plan<512, 16>;
@@ -177,7 +185,7 @@ __device__ __forceinline__ void fft512_warp(double2 (&v)[16], int lane, int c, c
     double2 u[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) u[r] = v[b + 2 * r];
-    radix8_twiddles<DIR>(u, tw + P::tw_offset(1) + l7, 8);
+    radix8_twiddles<DIR, LD>(u, tw + P::tw_offset(1) + l7, 8);
     Dft<8, DIR>::run(u);
     double2* wb = buf + 512 * ((lane >> 3) + 4 * b);
 #pragma unroll
@@ -191,28 +199,31 @@ __device__ __forceinline__ void fft512_warp(double2 (&v)[16], int lane, int c, c
 #pragma unroll
     for (int r = 0; r < 8; ++r) u[r] = v[b + 2 * r];
     const int k = lane + 32 * b;
-    radix8_twiddles<DIR>(u, tw + P::tw_offset(2) + k, 64);
+    radix8_twiddles<DIR, LD>(u, tw + P::tw_offset(2) + k, 64);
     Dft<8, DIR>::run(u);
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[b + 2 * r] = u[r];
   }
 }
 
-template <int L, int DIR>
+template <int L, int DIR, typename LD = LdgLoad>
 __device__ __forceinline__ void warp_fft(double2 (&v)[L / 32], int lane, const double2* __restrict__ tw,
                                          const SwzCol& col) {
   if constexpr (L == 512 && kFft512) {
-    fft512_warp<DIR>(v, lane, col.c, tw, col.buf);
+    fft512_warp<DIR, LD>(v, lane, col.c, tw, col.buf);
   } else {
+    static_assert(std::is_same<LD, LdgLoad>::value, "shared-memory tables: 512-point warp transform only");
     line_fft<L, DIR, L / 32>(v, lane, tw, col, SyncWarp{});
   }
 }
 
 // The warp's column: read (natural order), transform, write back.  o = outer
 // index (y of the x pass), z = the column's global z.
-template <int L, int KIND>
+template <int L, int KIND, typename LD = LdgLoad>
 __device__ __forceinline__ void column(const SwzCol& col, int lane, const double2* __restrict__ tw,
-                                       const PhaseArgs& ph, uint32_t o, uint32_t z) {
+                                       const PhaseArgs& ph, uint32_t o, uint32_t z,
+                                       const double2* sctk = nullptr) {
+  if constexpr (std::is_same<LD, LdgLoad>::value) sctk = ph.sctk;
   constexpr int E = L / 32;
   // element lane + 32 m of the column: row lane + 32 m, chunk c ^ (lane & 7)
   double2* const nb = col.buf + 8 * lane + (col.c ^ (lane & 7));
@@ -222,9 +233,9 @@ __device__ __forceinline__ void column(const SwzCol& col, int lane, const double
   __syncwarp();
   if constexpr (KIND == T_COPY) {  // diagnostics: the tile mover alone
   } else if constexpr (KIND == T_FWD) {
-    warp_fft<L, -1>(v, lane, tw, col);
+    warp_fft<L, -1, LD>(v, lane, tw, col);
   } else if constexpr (KIND == T_INV) {
-    warp_fft<L, +1>(v, lane, tw, col);
+    warp_fft<L, +1, LD>(v, lane, tw, col);
   } else {  // T_KIN
     double ky2, kz2;
     if (ph.kgen) {
@@ -234,7 +245,7 @@ __device__ __forceinline__ void column(const SwzCol& col, int lane, const double
       ky2 = __ldg(&ph.ky2[ph.outer_off + o]);
       kz2 = __ldg(&ph.kz2[ph.z_off + z]);
     }
-    warp_fft<L, -1>(v, lane, tw, col);
+    warp_fft<L, -1, LD>(v, lane, tw, col);
     // Lane t evaluates the factor of its point t + 32 q (q < E/2, index <
     // L/2).  Its point m = E - q has index L - ((32 - t) + 32 (q - 1)), the
     // mirror of lane 32 - t's point of iteration q - 1, received by shuffle;
@@ -244,14 +255,14 @@ __device__ __forceinline__ void column(const SwzCol& col, int lane, const double
     double2 shp = make_double2(0.0, 0.0);
 #pragma unroll
     for (int q = 0; q < E / 2; ++q) {
-      const double2 f = kfactor(kx2_of(lane + 32 * q, ph), ky2, kz2, ph);
+      const double2 f = kfactor<LD>(kx2_of(lane + 32 * q, ph), ky2, kz2, ph, sctk);
       apply_k(v[q], f, ph.imag);
       if (q >= 1) apply_k(v[E - q], lane == 0 ? f : shp, ph.imag);
       shp = shfl2(f, mirror);
     }
-    const double2 fn = kfactor(kx2_of(L / 2, ph), ky2, kz2, ph);
+    const double2 fn = kfactor<LD>(kx2_of(L / 2, ph), ky2, kz2, ph, sctk);
     apply_k(v[E / 2], lane == 0 ? fn : shp, ph.imag);
-    warp_fft<L, +1>(v, lane, tw, col);
+    warp_fft<L, +1, LD>(v, lane, tw, col);
   }
 #pragma unroll
   for (int m = 0; m < E; ++m) nb[256 * m] = v[m];
@@ -337,6 +348,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
   uint64_t* done = full + kBufs;
   uint32_t* cnt = reinterpret_cast<uint32_t*>(done + kBufs);  // columns finished per fill
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
   const uint32_t ntiles = a.n_outer * a.nchunk;
   const uint32_t nloc = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   auto coords = [&](uint32_t j, int& c0, int& o) {
@@ -504,8 +516,7 @@ static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw,
   auto k = ring_kernel<L, KIND, AXIS, NoPeers, L >= 1024 ? 2 : 1, W>;
   if constexpr (L == 512 && KIND == T_KIN)
     if (wpc == 2) k = ring_kernel<L, KIND, AXIS, NoPeers, 2, W>;
-  constexpr size_t smem =
-      (size_t)kBufs * L * W * sizeof(double2) + 2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t) + 1024;
+  constexpr size_t smem = (size_t)kBufs * L * W * sizeof(double2) + kRingBarBytes + 1024;
   static std::atomic<uint64_t> attr_done[2];
   if (cudaError_t e = ctap_smem_attr(k, smem, attr_done[wpc == 2 ? 1 : 0])) return e;
   const uint32_t ntiles = a.n_outer * a.nchunk;
@@ -549,8 +560,7 @@ static cudaError_t launch_ring_peers(const TileArgs& a, const void* in, int P, c
       return cudaErrorInvalidValue;
   }
   auto k = ring_kernel<L, T_KIN, 4, PeerMaps>;
-  constexpr size_t smem =
-      (size_t)kBufs * L * kCols * sizeof(double2) + 2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t) + 1024;
+  constexpr size_t smem = (size_t)kBufs * L * kCols * sizeof(double2) + kRingBarBytes + 1024;
   static std::atomic<uint64_t> attr_done{0};
   if (cudaError_t e = ctap_smem_attr(k, smem, attr_done)) return e;
   const uint32_t ntiles = a.n_outer * a.nchunk;

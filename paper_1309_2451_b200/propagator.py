@@ -95,6 +95,15 @@ class NativePlan:
     def advance(self, psi: torch.Tensor, n: int):
         _lib.call("ctap_advance", self.handle, psi.data_ptr(), int(n), _device.stream_handle())
 
+    def advance_observe(self, psi: torch.Tensor, n: int, xs: torch.Tensor, xb1, xb2, margin: int) -> torch.Tensor:
+        """n steps, then the observer sums fused into the segment-end pass
+        (ctap_advance_observe): [sum rho, left, middle, right, edge]."""
+        out = torch.empty(5, dtype=torch.float64, device=psi.device)
+        _lib.call("ctap_advance_observe", self.handle, psi.data_ptr(), int(n), xs.data_ptr(),
+                  None if xb1 is None else xb1.data_ptr(), None if xb2 is None else xb2.data_ptr(),
+                  int(margin), out.data_ptr(), _device.stream_handle())
+        return out
+
     def run_pass(self, kind: int, src: torch.Tensor, dst: torch.Tensor):
         _lib.call("ctap_pass", self.handle, int(kind), src.data_ptr(), dst.data_ptr(),
                   _device.stream_handle())
@@ -296,6 +305,44 @@ def event_schedule(n_steps: int, observers) -> list:
     return sorted(e for e in events if e <= n_steps)
 
 
+class _FusedObservation:
+    """Which observer event sums evolve_real asks the segment-end pass for:
+    the (partition, margin) of the first PopulationRecorder firing at the
+    event, else the margin of an EdgeMonitor (no partition).  Other observers
+    of the event hit the same cached sums or make their own reduction."""
+
+    def __init__(self, grid):
+        self.grid = grid
+        self._xs = None
+        self._bounds = {}
+
+    @property
+    def xs(self):
+        if self._xs is None:
+            self._xs = _device.to_device_f64(self.grid.x)
+        return self._xs
+
+    def bounds(self, part):
+        if part is None:
+            return None, None
+        key = id(part)
+        if key not in self._bounds:
+            self._bounds[key] = (part, _device.to_device_f64(part.xb1), _device.to_device_f64(part.xb2))
+        return self._bounds[key][1:]
+
+    @staticmethod
+    def request(firing):
+        from .observables import EdgeMonitor, PopulationRecorder
+
+        for obs in firing:
+            if isinstance(obs, PopulationRecorder):
+                return obs.partition, int(obs.margin_cells)
+        for obs in firing:
+            if isinstance(obs, EdgeMonitor):
+                return None, int(obs.margin_cells)
+        return None
+
+
 def evolve_real(psi, plan: StepPlan, n_steps: int, observers=()):
     """Propagate n_steps of real time with observers (propagator.py:134-173).
 
@@ -313,18 +360,27 @@ def evolve_real(psi, plan: StepPlan, n_steps: int, observers=()):
     stats = EvolveStats(n_steps=n_steps)
     schedule = event_schedule(n_steps, observers)
     w, foreign = _resident(psi)
+    fused = _FusedObservation(w.grid)
     t0 = _time.perf_counter()
     try:
         current = 0
         for ev in schedule:
+            firing = [obs for obs in observers if ev % obs.stride == 0 or ev == n_steps]
             if ev > current:
-                plan.native.advance(w.device_amplitudes(plan.native.torch_dtype), ev - current)
+                d = w.device_amplitudes(plan.native.torch_dtype)
+                req = fused.request(firing)
+                if req is None:
+                    plan.native.advance(d, ev - current)
+                else:  # the event's sums come out of the segment-end pass
+                    part, margin = req
+                    sums = plan.native.advance_observe(d, ev - current, fused.xs, *fused.bounds(part), margin)
                 w.time += (ev - current) * plan.dt
                 w.invalidate_norm()
+                if req is not None:
+                    w._obs_cache[int(margin)] = (part, sums.tolist())
                 current = ev
-            for obs in observers:
-                if ev % obs.stride == 0 or ev == n_steps:
-                    obs.notify(ev, w)
+            for obs in firing:
+                obs.notify(ev, w)
     finally:
         if torch.cuda.is_available():
             torch.cuda.synchronize()
