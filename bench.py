@@ -249,7 +249,9 @@ def run_ours(args):
         prop.transport = "nccl"
     else:
         prop = slab.SlabPropagator(grid, v_local, m, DT, transport=args.transport,
-                                   barrier=host_barrier if args.share_device else None)
+                                   barrier=host_barrier if args.share_device else None, chunks=args.chunks)
+        if prop.chunks > 1:
+            decomp += f", {prop.chunks} z chunks: chunk c's all-to-all overlaps chunk c+1's pass"
         if getattr(prop, "transport_fallback", None):
             decomp += f"; fused transport unavailable: {prop.transport_fallback}"
 
@@ -584,6 +586,8 @@ def main():
     ap.add_argument("--pencil-c", type=int, default=0, help="pencil columns Pc (default 4 at N >= 8, else 2)")
     ap.add_argument("--transport", choices=["nccl", "fused"], default="nccl",
                     help="slab transposes: NCCL all-to-all (default) or fused CUDA-IPC peer stores")
+    ap.add_argument("--chunks", type=int, default=4,
+                    help="slab NCCL transport: z chunks whose all-to-alls overlap the next chunk's pass (1: serial)")
     ap.add_argument("--share-device", action="store_true",
                     help="all ranks on cuda:0 over gloo: a launch test of the N-rank path on one GPU")
     ap.add_argument("--no-e2e", action="store_true")

@@ -179,6 +179,17 @@ CTAP_API int ctap_density_xz(ctap_plan* plan, const void* psi_dev, double* out_d
 CTAP_API int ctap_k2_sums(ctap_plan* plan, const void* phi_dev, double* out_dev, void* stream);
 CTAP_API int ctap_v_sums(ctap_plan* plan, const void* psi_dev, double* out_dev, void* stream);
 
+/* The slab kinetic block by z chunks (overlapped NCCL transport): kinds
+ * CTAP_PASS_Y_FWD_TO_PEER (psi columns [z0, z0+zn) -> send chunk),
+ * CTAP_PASS_X_KIN (recv chunk in place) and CTAP_PASS_Y_INV_FROM_PEER (send
+ * chunk -> psi columns) with CHUNK-MAJOR transpose buffers: the chunk's
+ * buffers are [peer][x_local][y_local][zn] and (nx, y_local, zn), so its
+ * all-to-all moves contiguous per-peer blocks while the next chunk computes.
+ * Bitwise equal to the unchunked passes.  zn a multiple of 8 dividing nz, z0
+ * a multiple of zn; slab plans (slab_p > 1) only. */
+CTAP_API int ctap_pass_zchunk(ctap_plan* plan, int32_t kind, const void* in, void* out, int64_t z0, int64_t zn,
+                              void* stream);
+
 /* Register, for the fused slab passes, the device addresses (as seen by this
  * process: peer-mapped through ctap_ipc_open, or local) of every rank's
  * buffers: which = 0: the y-slab buffers (nx, ny/P, nz) the y pass writes;

@@ -307,6 +307,22 @@ CTAP_API int ctap_pass(ctap_plan* p, int32_t kind, const void* in, void* out, vo
   return CTAP_OK;
 }
 
+CTAP_API int ctap_pass_zchunk(ctap_plan* p, int32_t kind, const void* in, void* out, int64_t z0, int64_t zn,
+                              void* stream) {
+  Range nvtx("ctap_pass_zchunk %lld", kind);
+  if (!p || !in || !out) return fail(CTAP_EINVAL, "null argument");
+  if (p->slab_p < 2 || p->pen_c) return fail(CTAP_EINVAL, "z-chunked passes serve slab plans (slab_p > 1)");
+  if (kind != CTAP_PASS_Y_FWD_TO_PEER && kind != CTAP_PASS_X_KIN && kind != CTAP_PASS_Y_INV_FROM_PEER)
+    return fail(CTAP_EINVAL, "pass %d has no z-chunked form", kind);
+  if (zn <= 0 || zn % 8 || z0 < 0 || z0 + zn > p->n[2] || z0 % zn)
+    return fail(CTAP_EINVAL, "z chunk [%lld, %lld) must be a multiple-of-8 slice of nz = %lld",
+                (long long)z0, (long long)(z0 + zn), (long long)p->n[2]);
+  if (kind == CTAP_PASS_X_KIN && (in != out || p->expk_dev))
+    return fail(CTAP_EINVAL, "z-chunked kinetic pass runs in place without the exp(-ik^2dt/2) table");
+  CUDA_TRY(ctap_run_pass_chunk(p, kind, in, out, z0, zn, (cudaStream_t)stream), "ctap_pass_zchunk");
+  return CTAP_OK;
+}
+
 // y, [x K x^-1], y^-1 of one step.  With p->zchunk = W the three passes run
 // per z chunk of W columns, so a chunk (nx ny W points) stays in L2 from the
 // y pass to the y^-1 pass instead of making three HBM round trips.
@@ -420,7 +436,7 @@ CTAP_API int ctap_advance_observe(ctap_plan* p, void* psi, int64_t n, const doub
   p->skip_last = 0;
   if (rc != CTAP_OK) return rc;
   CUDA_TRY(ctap_run_z_last_observe(p, psi, xs, xb1, xb2, margin, p->obs_partial, st), "ctap_advance_observe");
-  CUDA_TRY(ctap_run_finalize5(p->obs_partial, ctap_z_blocks(p), out, st), "ctap_advance_observe");
+  CUDA_TRY(ctap_run_finalize5(p, p->obs_partial, ctap_z_blocks(p), out, st), "ctap_advance_observe");
   return CTAP_OK;
 }
 

@@ -105,9 +105,12 @@ namespace ctap {
 struct ZArgs;
 }
 int64_t ctap_z_blocks(const ctap_plan* p);
+cudaError_t ctap_run_pass_chunk(const ctap_plan* p, int kind, const void* in, void* out, int64_t z0, int64_t zn,
+                                cudaStream_t st);
 cudaError_t ctap_run_z_last_observe(const ctap_plan* p, void* psi, const double* xs, const double* xb1,
                                     const double* xb2, int margin, double* partial, cudaStream_t st);
-cudaError_t ctap_run_finalize5(const double* partial, int64_t nblocks, double* out, cudaStream_t st);
+cudaError_t ctap_run_finalize5(const ctap_plan* p, const double* partial, int64_t nblocks, double* out,
+                               cudaStream_t st);
 cudaError_t ctap_run_z2(const ctap_plan* p, int tkind, bool vtab, int ch, const ctap::ZArgs& a, cudaStream_t st);
 static inline int ilog2i(int64_t v) {
   int l = 0;

@@ -842,3 +842,80 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
   }
   return cudaErrorInvalidValue;
 }
+
+// Slab kinetic block by z chunks (the overlapped NCCL transport): the passes
+// of one chunk of zn columns [z0, z0 + zn) with CHUNK-MAJOR transpose
+// buffers, so each chunk's all-to-all moves contiguous per-peer blocks and can
+// run while the next chunk's pass computes (z is untouched by y, x and the
+// kinetic factor, so chunks are independent through the block):
+//   Y_FWD_TO_PEER   psi columns [z0, z0 + zn) -> send chunk [peer][x_l][y_l][zn]
+//   X_KIN           recv chunk (nx, y_l, zn) in place, kz offset z0
+//   Y_INV_FROM_PEER send chunk [peer][x_l][y_l][zn] -> psi columns [z0, z0 + zn)
+// The per-line arithmetic is the unchunked passes', so results are bitwise
+// equal to them (tests/test_gpu_slab_virtual.py).
+cudaError_t ctap_run_pass_chunk(const ctap_plan* p, int kind, const void* in, void* out, int64_t z0, int64_t zn,
+                                cudaStream_t st) {
+  const int64_t nx = p->n[0], ny = p->n[1], nz = p->n[2];
+  const int P = p->slab_p;
+  if (P < 2 || p->pen_c || zn <= 0 || (zn & 7) || z0 < 0 || z0 + zn > nz) return cudaErrorInvalidValue;
+  const bool c64 = p->dtype == CTAP_C64;
+  const size_t csz = c64 ? sizeof(float2) : sizeof(double2);
+  const uint32_t nxl = (uint32_t)(nx / P), nyl = (uint32_t)(ny / P);
+  const uint32_t NZ = (uint32_t)nz, NY = (uint32_t)ny, ZN = (uint32_t)zn;
+  constexpr int kNone = 31;
+  TileArgs a;
+  a.nchunk = ZN / 8;
+  PhaseArgs& ph = a.ph;
+  ph.vi = p->vi_dev;
+  ph.expv = p->expv_dev;
+  ph.kx2 = p->k2_dev[0];
+  ph.ky2 = p->k2_dev[1];
+  ph.kz2 = p->k2_dev[2];
+  ph.expk = nullptr;
+  ph.len2 = p->len2;
+  ph.dt_i = p->dt_i;
+  ph.scale = p->inv_scale;
+  ph.imag = p->mode == 1;
+  ph.outer_off = 0;
+  ph.kgen = p->kgen;
+  ph.sct = p->sctab;
+  ph.sctk = p->sctab + kSCN;
+  ph.z_off = (uint32_t)z0;
+  for (int i = 0; i < 3; ++i) {
+    ph.kn[i] = (uint32_t)p->n[i];
+    ph.kval[i] = p->kval[i];
+  }
+  const Layout y_nat{NY * NZ, 0u, NZ, 0, 0u, kNone};
+  const Layout y_peer_c{nyl * ZN, nxl * nyl * ZN, ZN, ilog2(nyl), 0u, kNone};
+  const Layout x_nat_c{ZN, 0u, nyl * ZN, 0, 0u, kNone};
+  switch (kind) {
+    case PASS_Y_FWD_TO_PEER:
+      a.in = (const char*)in + csz * (size_t)z0;
+      a.out = out;
+      a.n_outer = nxl;
+      a.lin = y_nat;
+      a.lout = y_peer_c;
+      return dispatch_tile<T_FWD, false, true, false>((int)ny, c64, a, twid(p, ny), st);
+    case PASS_Y_INV_FROM_PEER:
+      a.in = in;
+      a.out = (char*)out + csz * (size_t)z0;
+      a.n_outer = nxl;
+      a.lin = y_peer_c;
+      a.lout = y_nat;
+      return dispatch_tile<T_INV, true, false, false>((int)ny, c64, a, twid(p, ny), st);
+    case PASS_X_KIN: {
+      if (in != out || p->expk_dev) return cudaErrorInvalidValue;
+      a.in = in;
+      a.out = out;
+      a.n_outer = nyl;
+      a.lin = a.lout = x_nat_c;
+      a.ph.outer_off = (uint32_t)p->slab_r * nyl;
+      if (!c64) {
+        cudaError_t e = ctap_run_wline(p, 2, T_KIN, p->wline, out, a, st);
+        if (e != cudaErrorNotSupported) return e;
+      }
+      return dispatch_tile<T_KIN, false, false, false>((int)nx, c64, a, twid(p, nx), st);
+    }
+  }
+  return cudaErrorInvalidValue;
+}

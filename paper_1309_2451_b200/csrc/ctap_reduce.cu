@@ -209,10 +209,21 @@ static cudaError_t k2_t(const ctap_plan* p, const void* phi, double* out, cudaSt
   return run_reduce<2>(p, f, p->n[0] * f.nylz, out, st);
 }
 
-// fixed-order sum of the fused z pass's block partials (ctap_advance_observe)
-cudaError_t ctap_run_finalize5(const double* partial, int64_t nblocks, double* out, cudaStream_t st) {
-  finalize_kernel<5><<<1, kRedThreads, 0, st>>>(partial, (int)nblocks, out);
-  return cudaGetLastError();
+struct PartialF {  // the fused z pass's block partials, 5 per block
+  const double* partial;
+  __device__ __forceinline__ void operator()(int64_t i, double (&acc)[5]) const {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc[k] += partial[i * 5 + k];
+  }
+};
+
+// fixed-order sum of the fused z pass's block partials (ctap_advance_observe):
+// the same two-stage grid reduction as the observer sums (a single block
+// walking 65536 partials would be latency-bound: ~0.4 ms at 512^3)
+cudaError_t ctap_run_finalize5(const ctap_plan* p, const double* partial, int64_t nblocks, double* out,
+                               cudaStream_t st) {
+  PartialF f{partial};
+  return run_reduce<5>(p, f, nblocks, out, st);
 }
 
 cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, cudaStream_t st) {

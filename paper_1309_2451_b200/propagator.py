@@ -108,6 +108,12 @@ class NativePlan:
         _lib.call("ctap_pass", self.handle, int(kind), src.data_ptr(), dst.data_ptr(),
                   _device.stream_handle())
 
+    def run_pass_zchunk(self, kind: int, src: torch.Tensor, dst: torch.Tensor, z0: int, zn: int):
+        """A slab pass on z columns [z0, z0 + zn) with chunk-major transpose
+        buffers (ctap_pass_zchunk)."""
+        _lib.call("ctap_pass_zchunk", self.handle, int(kind), src.data_ptr(), dst.data_ptr(), int(z0), int(zn),
+                  _device.stream_handle())
+
     def run_pass_ptr(self, kind: int, src: int, dst: int):
         """A pass on raw device addresses (plan-external buffers)."""
         _lib.call("ctap_pass", self.handle, int(kind), src, dst, _device.stream_handle())

@@ -123,6 +123,31 @@ def segment_schedule_fused(n_steps: int):
         yield ("pass", _lib.PASS_Z_MID if j < n_steps - 1 else _lib.PASS_Z_LAST, "psi", "psi")
 
 
+def segment_schedule_chunked(n_steps: int, chunks: int):
+    """The same n merged steps with the kinetic block split into `chunks` z
+    chunks (chunk-major transpose buffers, ctap_pass_zchunk): ops
+    ('pass', kind, src, dst), ('cpass', kind, src, dst, c) and
+    ('a2a', src, dst, c).  Listed in issue order: all y passes, then the
+    chunks' all-to-alls, ... so chunk c's transfer overlaps chunk c+1's pass
+    when passes and transfers run on two streams."""
+    if n_steps <= 0:
+        return
+    yield ("pass", _lib.PASS_Z_FIRST, "psi", "psi")
+    C = range(chunks)
+    for j in range(n_steps):
+        for c in C:
+            yield ("cpass", _lib.PASS_Y_FWD_TO_PEER, "psi", "send", c)
+        for c in C:
+            yield ("a2a", "send", "recv", c)
+        for c in C:
+            yield ("cpass", _lib.PASS_X_KIN, "recv", "recv", c)
+        for c in C:
+            yield ("a2a", "recv", "send", c)
+        for c in C:
+            yield ("cpass", _lib.PASS_Y_INV_FROM_PEER, "send", "psi", c)
+        yield ("pass", _lib.PASS_Z_MID if j < n_steps - 1 else _lib.PASS_Z_LAST, "psi", "psi")
+
+
 class DeviceBuffer:
     """cudaMalloc'd buffer owned by libctap (exportable through CUDA IPC)."""
 
@@ -181,7 +206,7 @@ class SlabPropagator:
 
     def __init__(self, grid, v_local, mass: float, dt: float, group=None, mode: str = REAL_TIME,
                  v_shift: float = 0.0, phase_tables: int | None = None, precision: str = "complex128",
-                 transport: str = "nccl", barrier=None):
+                 transport: str = "nccl", barrier=None, chunks: int = 1):
         self.grid = as_simgrid(grid)
         self.group = group
         self._barrier_fn = barrier  # fused transport: default is a 1-float NCCL all-reduce
@@ -210,6 +235,12 @@ class SlabPropagator:
         if self.transport == "nccl":
             self.send = torch.empty(self.layout.points, dtype=dt_, device=dev)
             self.recv = torch.empty(self.layout.points, dtype=dt_, device=dev)
+        # NCCL transport by z chunks: chunk c's all-to-all on a second stream
+        # overlaps chunk c+1's pass (chunk-major buffers, ctap_pass_zchunk)
+        nz = self.grid.n[2]
+        self.chunks = int(chunks) if (self.transport == "nccl" and P > 1 and chunks > 1
+                                      and nz % (8 * int(chunks)) == 0 and not (self.phase_tables & 2)) else 1
+        self._comm = torch.cuda.Stream(device=dev) if self.chunks > 1 and dev.type == "cuda" else None
 
     def _setup_fused(self, dtype) -> bool:
         """Allocate this rank's y-slab and peer-major buffers, exchange CUDA IPC
@@ -317,6 +348,9 @@ class SlabPropagator:
                 else:
                     self._barrier()
             return
+        if self.chunks > 1:
+            self._advance_chunked(psi_local, n_steps)
+            return
         bufs = {"psi": psi_local.reshape(-1), "send": self.send, "recv": self.recv}
         for op in segment_schedule(n_steps):
             if op[0] == "pass":
@@ -324,6 +358,41 @@ class SlabPropagator:
                 self.native.run_pass(kind, bufs[src], bufs[dst])
             else:
                 self._a2a(bufs[op[1]], bufs[op[2]])
+
+    def _advance_chunked(self, psi_local: torch.Tensor, n_steps: int):
+        """segment_schedule_chunked on two streams: passes on the current
+        stream, all-to-alls on the plan's comm stream, event-ordered per chunk."""
+        K = self.chunks
+        W = self.grid.n[2] // K
+        csz = self.layout.points // K
+        psi = psi_local.reshape(-1)
+        bufs = {"send": self.send, "recv": self.recv}
+        main = torch.cuda.current_stream()
+        comm = self._comm
+        ready = {}  # (buffer, chunk) -> event after which that chunk's data is complete
+        for op in segment_schedule_chunked(n_steps, K):
+            if op[0] == "pass":
+                self.native.run_pass(op[1], psi, psi)
+            elif op[0] == "cpass":
+                _, kind, src, dst, c = op
+                if (src, c) in ready:
+                    main.wait_event(ready.pop((src, c)))
+                s_ = psi if src == "psi" else bufs[src][c * csz:(c + 1) * csz]
+                d_ = psi if dst == "psi" else bufs[dst][c * csz:(c + 1) * csz]
+                self.native.run_pass_zchunk(kind, s_, d_, c * W, W)
+                if dst != "psi":
+                    ev = torch.cuda.Event()
+                    ev.record(main)
+                    ready[(dst, c)] = ev
+            else:
+                _, src, dst, c = op
+                comm.wait_event(ready.pop((src, c)))
+                with torch.cuda.stream(comm):
+                    all_to_all_c(bufs[dst][c * csz:(c + 1) * csz], bufs[src][c * csz:(c + 1) * csz], self.group)
+                    ev = torch.cuda.Event()
+                    ev.record(comm)
+                ready[(dst, c)] = ev
+        main.wait_stream(comm)
 
     def observe(self, psi_local: torch.Tensor, xb1=None, xb2=None, margin: int = 2) -> list:
         """Global [sum rho, left, middle, right, edge] (raw sums, rank-ordered)."""

@@ -156,3 +156,48 @@ def _lib_pass(name):
     from paper_1309_2451_b200 import _lib
 
     return getattr(_lib, name)
+
+
+def run_virtual_chunked(grid, v, a0, P, steps, K):
+    """The NCCL transport by z chunks (segment_schedule_chunked, chunk-major
+    buffers, ctap_pass_zchunk) with the all-to-alls emulated chunk by chunk."""
+    from paper_1309_2451_b200.slab import segment_schedule_chunked
+
+    lays = [SlabLayout(grid.n, P, r) for r in range(P)]
+    vs = [torch.from_numpy(np.ascontiguousarray(v[l.x_slice])).cuda() for l in lays]
+    plans = [NativePlan(grid, vs[r], M, 1e-6, slab_p=P, slab_r=r) for r in range(P)]
+    bufs = [{"psi": torch.from_numpy(np.ascontiguousarray(a0[l.x_slice])).cuda().reshape(-1),
+             "send": torch.empty(l.points, dtype=torch.complex128, device="cuda"),
+             "recv": torch.empty(l.points, dtype=torch.complex128, device="cuda")} for l in lays]
+    W = grid.n[2] // K
+    csz = lays[0].points // K        # one chunk of a rank's buffer
+    blk = csz // P                   # one peer's block inside a chunk
+    for op in segment_schedule_chunked(steps, K):
+        if op[0] == "pass":
+            for r in range(P):
+                plans[r].run_pass(op[1], bufs[r][op[2]], bufs[r][op[3]])
+        elif op[0] == "cpass":
+            _, kind, src, dst, c = op
+            for r in range(P):
+                s_ = bufs[r]["psi"] if src == "psi" else bufs[r][src][c * csz:(c + 1) * csz]
+                d_ = bufs[r]["psi"] if dst == "psi" else bufs[r][dst][c * csz:(c + 1) * csz]
+                plans[r].run_pass_zchunk(kind, s_, d_, c * W, W)
+        else:
+            _, src, dst, c = op
+            for q in range(P):
+                for p in range(P):
+                    bufs[q][dst][c * csz + p * blk:c * csz + (p + 1) * blk].copy_(
+                        bufs[p][src][c * csz + q * blk:c * csz + (q + 1) * blk])
+    return torch.cat([b["psi"] for b in bufs]).reshape(grid.n).cpu().numpy()
+
+
+@pytest.mark.parametrize("P,K,n", [(2, 2, (32, 16, 32)), (4, 4, (32, 16, 64)), (2, 4, (512, 8, 64)),
+                                   (8, 2, (64, 16, 32))])
+def test_virtual_slabs_zchunked_bitwise_equal_single_gpu(P, K, n):
+    """The overlapped NCCL transport's chunked passes and per-chunk exchanges
+    give bitwise the single-GPU propagation (and the unchunked slab's)."""
+    grid, v, a0 = _case(n)
+    got = run_virtual_chunked(grid, v, a0, P, 5, K)
+    psi = qgrid.Wavefunction(a0.copy(), grid)
+    psi, _ = propagator.evolve_real(psi, propagator.make_plan(grid, v, M, 1e-6), 5)
+    assert np.array_equal(got, psi.amplitudes)

@@ -131,3 +131,28 @@ def test_fused_schedule_shape():
                      _lib.PASS_Y_INV_FROM_PEER, _lib.PASS_Z_MID,
                      _lib.PASS_Y_FWD_TO_PEERS, "barrier", _lib.PASS_X_KIN_TO_PEERS, "barrier",
                      _lib.PASS_Y_INV_FROM_PEER, _lib.PASS_Z_LAST]
+
+
+def test_chunked_schedule_shape_and_dependencies():
+    """segment_schedule_chunked: per step K y passes, K exchanges, K kinetic
+    passes, K exchanges, K y^-1 passes; every chunk's exchange comes after its
+    own producer pass and before its consumer pass (the event order the two
+    streams of SlabPropagator._advance_chunked follow)."""
+    from paper_1309_2451_b200 import _lib
+    from paper_1309_2451_b200.slab import segment_schedule_chunked
+
+    K, steps = 4, 2
+    ops = list(segment_schedule_chunked(steps, K))
+    assert ops[0] == ("pass", _lib.PASS_Z_FIRST, "psi", "psi") and ops[-1][1] == _lib.PASS_Z_LAST
+    assert sum(1 for o in ops if o[0] == "a2a") == 2 * K * steps
+    assert sum(1 for o in ops if o[0] == "cpass") == 3 * K * steps
+    done = set()
+    for o in ops:
+        if o[0] == "cpass":
+            _, kind, src, dst, c = o
+            if src != "psi":
+                assert (src, c) in done, o
+            done.add((dst, c))
+        elif o[0] == "a2a":
+            assert (o[1], o[3]) in done, o
+            done.add((o[2], o[3]))
