@@ -337,7 +337,7 @@ def run_ours(args):
         xs_d = torch.from_numpy(grid.axis(0)).to(dev)
         xb = (torch.from_numpy(part.xb1).to(dev), torch.from_numpy(part.xb2).to(dev))
 
-        def timed(fn, reps=5):
+        def timed(fn, reps=10):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             a.record(stream)
@@ -355,7 +355,7 @@ def run_ours(args):
         for f in (plain, fusedo, separate):
             f()
         d_f, d_s, t_p = [], [], []
-        for _ in range(7):
+        for _ in range(9):
             tp, tf, ts = timed(plain), timed(fusedo), timed(separate)
             t_p.append(tp)
             d_f.append(tf - tp)
@@ -363,7 +363,7 @@ def run_ours(args):
         obs_cost = {"segment_steps": 1, "segment_ms": statistics.median(t_p),
                     "extra_ms_fused": statistics.median(d_f),
                     "extra_ms_standalone_reduction": statistics.median(d_s),
-                    "method": "CUDA events, 1-step segments x 5, the variants interleaved, median of 7"}
+                    "method": "CUDA events, 1-step segments x 10, the variants interleaved, median of 9"}
     dom_name = max(per_pass, key=lambda k: per_pass[k]["ms"])
     dom = per_pass[dom_name]
     peak, peak_kind = _peaks()

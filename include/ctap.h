@@ -143,8 +143,9 @@ CTAP_API int ctap_advance(ctap_plan* plan, void* psi_dev, int64_t n_steps, void*
 /* evolve_real's segment + observer event (propagator.py:160-168): n telescoped
  * steps, then the raw sums of ctap_observe ([sum rho, left, middle, right,
  * edge(margin)] into out_dev[5]) -- computed inside the segment-end pass
- * [z^-1 . Vh] from the registers it writes psi from (block partials, summed
- * in a fixed order), so the event reads no extra byte of psi.  n == 0 (or an
+ * [z^-1 . Vh] from the registers it writes psi from (warp partials summed in
+ * a fixed order; the middle guide as total - left - right), so the event
+ * reads no extra byte of psi.  n == 0 (or an
  * imaginary-time plan) runs the standalone ctap_observe.  xs/xb1/xb2 as for
  * ctap_observe (device pointers; xb1 = xb2 = NULL: no partition). */
 CTAP_API int ctap_advance_observe(ctap_plan* plan, void* psi_dev, int64_t n_steps, const double* xs,

@@ -428,7 +428,7 @@ CTAP_API int ctap_advance_observe(ctap_plan* p, void* psi, int64_t n, const doub
     return CTAP_OK;
   }
   if (!p->obs_partial)
-    CUDA_TRY(cudaMalloc((void**)&p->obs_partial, sizeof(double) * 5 * ctap_z_blocks(p)), "ctap_advance_observe");
+    CUDA_TRY(cudaMalloc((void**)&p->obs_partial, sizeof(double) * 4 * ctap_z_blocks(p)), "ctap_advance_observe");
   // all but the last pass of the segment: ctap_advance of n steps minus its
   // final [z^-1 . Vh] (the same launches, graphs included)
   p->skip_last = 1;
@@ -436,7 +436,7 @@ CTAP_API int ctap_advance_observe(ctap_plan* p, void* psi, int64_t n, const doub
   p->skip_last = 0;
   if (rc != CTAP_OK) return rc;
   CUDA_TRY(ctap_run_z_last_observe(p, psi, xs, xb1, xb2, margin, p->obs_partial, st), "ctap_advance_observe");
-  CUDA_TRY(ctap_run_finalize5(p, p->obs_partial, ctap_z_blocks(p), out, st), "ctap_advance_observe");
+  CUDA_TRY(ctap_run_finalize5(p, p->obs_partial, ctap_z_blocks(p), out, xb1 != nullptr, st), "ctap_advance_observe");
   return CTAP_OK;
 }
 

@@ -109,8 +109,8 @@ cudaError_t ctap_run_pass_chunk(const ctap_plan* p, int kind, const void* in, vo
                                 cudaStream_t st);
 cudaError_t ctap_run_z_last_observe(const ctap_plan* p, void* psi, const double* xs, const double* xb1,
                                     const double* xb2, int margin, double* partial, cudaStream_t st);
-cudaError_t ctap_run_finalize5(const ctap_plan* p, const double* partial, int64_t nblocks, double* out,
-                               cudaStream_t st);
+cudaError_t ctap_run_finalize5(const ctap_plan* p, const double* partial, int64_t npartials, double* out,
+                               int part, cudaStream_t st);
 cudaError_t ctap_run_z2(const ctap_plan* p, int tkind, bool vtab, int ch, const ctap::ZArgs& a, cudaStream_t st);
 static inline int ilog2i(int64_t v) {
   int l = 0;

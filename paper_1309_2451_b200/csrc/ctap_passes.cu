@@ -122,50 +122,51 @@ struct ZMinBlocks {
   static constexpr int value = (KIND == T_VMID && VTAB) ? CTAP_Z_MINB_TAB : CTAP_Z_MINB;
 };
 
-// The five observer sums of this thread's points (psi after the segment-end
-// pass, in registers), reduced over the block in a fixed order and stored as
-// the block's partial: the reduction of observables.py:74-110 fused into the
-// write-back of the last pass, so an observer event reads no extra byte of
-// psi.  Deterministic: fixed per-thread order, shuffle tree,
-// warp order; the finalize sums the block partials in a fixed order.
+// The observer sums of this thread's points (psi after the segment-end pass,
+// in registers), reduced over the warp in a fixed shuffle tree and stored as
+// the warp's partial [sum rho, left, right, edge]: the reduction of
+// observables.py:74-110 fused into the write-back of the last pass, so an
+// observer event reads no extra byte of psi.  The middle guide
+// is total - left - right, formed in the finalize (ctap_reduce.cu).
+// Deterministic: fixed per-thread order, shuffle tree, partial order.
+constexpr int kObsVals = 4;
 template <int L, typename CV>
 __device__ __forceinline__ void z_observe(const ZArgs& a, const CV* v, int t, uint32_t line, bool active) {
   constexpr int T = L / kElems;
-  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  double acc[kObsVals] = {0.0, 0.0, 0.0, 0.0};
   if (active) {
     const uint32_t x = line / a.ny, y = line - x * a.ny;
     const int mg = a.margin;
     const bool line_edge = (int)x < mg || (int)x >= (int)a.nx - mg || (int)y < mg || (int)y >= (int)a.ny - mg;
     const double xv = __ldg(&a.xs[x]);
+    const bool part = a.xb1 != nullptr;
 #pragma unroll
     for (int m = 0; m < kElems; ++m) {
       const int z = t + m * T;
       const double rho = (double)v[m].x * v[m].x + (double)v[m].y * v[m].y;
       acc[0] += rho;
-      if (a.xb1 != nullptr) {
-        const bool in_l = xv < __ldg(&a.xb1[z]);
-        const bool in_r = xv >= __ldg(&a.xb2[z]);
-        if (in_l) acc[1] += rho;
-        if (in_r) acc[3] += rho;
-        if (!(in_l || in_r)) acc[2] += rho;
+      if (part) {
+        if (xv < __ldg(&a.xb1[z])) acc[1] += rho;
+        if (xv >= __ldg(&a.xb2[z])) acc[2] += rho;
       }
-      if (line_edge || z < mg || z >= L - mg) acc[4] += rho;
+      // z-edge points: for margin <= T only the first and last of a thread's
+      // points can be within margin of a z face
+      if (m == 0 || m == kElems - 1 || mg > T)
+        if (z < mg || z >= L - mg) acc[3] += rho;
     }
+    if (line_edge) acc[3] = acc[0];  // every point of the line: the same sum in the same order
   }
-  __shared__ double sh[5][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    double s = acc[k];
+  for (int k = 0; k < kObsVals; ++k) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) sh[k][warp] = s;
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
   }
-  __syncthreads();
-  if (threadIdx.x < 5) {
-    double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[threadIdx.x][w];
-    a.obs_partial[(size_t)blockIdx.x * 5 + threadIdx.x] = s;
+  const int lane = threadIdx.x & 31;
+  if (lane < kObsVals) {
+    double r = acc[0];
+#pragma unroll
+    for (int k = 1; k < kObsVals; ++k) r = lane == k ? acc[k] : r;
+    a.obs_partial[((size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kObsVals + lane] = r;
   }
 }
 
@@ -476,12 +477,13 @@ cudaError_t ctap_run_pass(const ctap_plan* p, int kind, const void* in, void* ou
   return ctap_run_pass_z(p, kind, in, out, 0, p->n[2], st);
 }
 
-// number of blocks (= partials) of the segment-end z pass
+// number of warps (= observer partials, kObsVals each) of the segment-end z pass
 int64_t ctap_z_blocks(const ctap_plan* p) {
   const int64_t nlines = p->nx_local * p->n[1];
   const int T = (int)(p->n[2] / kElems);
   const int C = (CTAP_Z_THREADS / T) > 0 ? (CTAP_Z_THREADS / T) : 1;
-  return (nlines + C - 1) / C;
+  const int threads = C * T;
+  return (nlines + C - 1) / C * ((threads + 31) / 32);
 }
 
 // [z^-1 . Vh] with the observer sums fused (single-GPU plans): block partials

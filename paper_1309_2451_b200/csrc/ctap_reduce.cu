@@ -209,21 +209,39 @@ static cudaError_t k2_t(const ctap_plan* p, const void* phi, double* out, cudaSt
   return run_reduce<2>(p, f, p->n[0] * f.nylz, out, st);
 }
 
-struct PartialF {  // the fused z pass's block partials, 5 per block
+struct PartialF {  // the fused z pass's warp partials [total, left, right, edge]
   const double* partial;
-  __device__ __forceinline__ void operator()(int64_t i, double (&acc)[5]) const {
+  __device__ __forceinline__ void operator()(int64_t i, double (&acc)[4]) const {
 #pragma unroll
-    for (int k = 0; k < 5; ++k) acc[k] += partial[i * 5 + k];
+    for (int k = 0; k < 4; ++k) acc[k] += partial[i * 4 + k];
   }
 };
 
-// fixed-order sum of the fused z pass's block partials (ctap_advance_observe):
-// the same two-stage grid reduction as the observer sums (a single block
-// walking 65536 partials would be latency-bound: ~0.4 ms at 512^3)
-cudaError_t ctap_run_finalize5(const ctap_plan* p, const double* partial, int64_t nblocks, double* out,
-                               cudaStream_t st) {
+// [total, left, right, edge] -> [total, left, total - left - right, right, edge]
+// (no partition: the guide sums are 0, as ctap_observe reports them)
+__global__ void obs_layout_kernel(const double* __restrict__ s4, double* __restrict__ out, int part) {
+  if (threadIdx.x == 0) {
+    const double t = s4[0], l = s4[1], r = s4[2], e = s4[3];
+    out[0] = t;
+    out[1] = l;
+    out[2] = part ? (t - l) - r : 0.0;
+    out[3] = r;
+    out[4] = e;
+  }
+}
+
+// fixed-order sum of the fused z pass's warp partials (ctap_advance_observe):
+// the two-stage grid reduction of the observer sums (a single block walking
+// the partials would be latency-bound: ~0.4 ms at 512^3), then the middle
+// guide as total - left - right
+cudaError_t ctap_run_finalize5(const ctap_plan* p, const double* partial, int64_t npartials, double* out,
+                               int part, cudaStream_t st) {
   PartialF f{partial};
-  return run_reduce<5>(p, f, nblocks, out, st);
+  double* s4 = p->red_partial + 8 * (int64_t)p->red_blocks - 8;  // past the grid partials (red_blocks x 4 used)
+  cudaError_t e = run_reduce<4>(p, f, npartials, s4, st);
+  if (e != cudaSuccess) return e;
+  obs_layout_kernel<<<1, 32, 0, st>>>(s4, out, part);
+  return cudaGetLastError();
 }
 
 cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, cudaStream_t st) {
