@@ -158,3 +158,20 @@ def test_bench_thread_counts_matches_reference_rule():
     assert bench_thread_counts(6) == [1, 2, 4, 6]
     assert bench_thread_counts(8) == [1, 2, 4, 8]
     assert bench_thread_counts(16) == [1, 2, 4, 8, 16]
+
+
+def test_bench_grid_parsing_and_identical_arm_configs():
+    """bench.py: --grid parsing, and both arms report the same config dict
+    (the driver compares the arms' configs)."""
+    import argparse
+
+    import bench
+
+    assert bench.parse_grid("512x512x512") == (512, 512, 512)
+    assert bench.parse_grid("1024,1024,512") == (1024, 1024, 512)
+    with pytest.raises(argparse.ArgumentTypeError):
+        bench.parse_grid("64x64")
+    c = bench._config((512, 512, 512))
+    assert c == bench._config([512, 512, 512])
+    assert "BASELINE config 4" in c["workload"] and c["grid"] == [512, 512, 512]
+    assert "BASELINE config 5" in bench._config((1024, 1024, 512))["workload"]
