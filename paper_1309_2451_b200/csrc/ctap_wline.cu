@@ -51,6 +51,16 @@ constexpr int kGroups = CTAP_WL_GROUPS;  // ring: tiles in computation at once
 constexpr int kBufs = 3;    // ring: tile buffers
 constexpr int kRingThreads = kGroups * kCols * 32;  // 2 groups: 16 warps, 4 per SM sub-partition, 128 registers each
 constexpr int kTileThreads = kCols * 32;
+// TMA box height (rows per cp.async.bulk.tensor request) and L2 promotion of
+// the ring's tensor maps (A/B switches; 256 rows and 256-byte promotion by default)
+#ifndef CTAP_WL_BOX
+#define CTAP_WL_BOX 256
+#endif
+constexpr int kBoxRows = CTAP_WL_BOX;
+#ifndef CTAP_WL_PROMO
+#define CTAP_WL_PROMO 3
+#endif
+constexpr CUtensorMapL2promotion kL2Promo = (CUtensorMapL2promotion)CTAP_WL_PROMO;
 // full/done mbarriers + fill counters of the ring, padded to 16 bytes
 constexpr size_t kRingBarBytes = ((2 * kBufs * sizeof(uint64_t) + kBufs * sizeof(uint32_t)) + 15) / 16 * 16;
 #ifndef CTAP_FFT512
@@ -339,7 +349,7 @@ template <int L, int KIND, int AXIS, typename PM, int WPC = 1, int W = kCols>
 __global__ void __launch_bounds__(kRingThreads, 1)
     ring_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a, const double2* __restrict__ tw,
                 const __grid_constant__ PM pm) {
-  constexpr int BOX = L < 256 ? L : 256;
+  constexpr int BOX = L < kBoxRows ? L : kBoxRows;
   constexpr uint32_t kTileBytes = (uint32_t)L * W * sizeof(double2);
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);  // swizzle atom: 1 KB
@@ -495,7 +505,7 @@ static int sm_count() { return ctap_sm_count(); }
 // (n_outer, L, nz) array (nz = 8 * a.nchunk)
 template <int L, int KIND, int AXIS>
 static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw, cudaStream_t st, int wpc = 1) {
-  constexpr int BOX = L < 256 ? L : 256;
+  constexpr int BOX = L < kBoxRows ? L : kBoxRows;
   // 1024-point lines: 4-column tiles (64 KB), two warps per column
   constexpr int W = L >= 1024 ? 4 : kCols;
   if (L >= 1024) wpc = 2;
@@ -511,7 +521,7 @@ static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw,
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, data, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, W == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   kL2Promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   auto k = ring_kernel<L, KIND, AXIS, NoPeers, L >= 1024 ? 2 : 1, W>;
   if constexpr (L == 512 && KIND == T_KIN)
@@ -530,7 +540,7 @@ static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw,
 // (peer-major (nx/P, ny/P, nz) block of this rank inside rank q's buffer).
 template <int L>
 static cudaError_t launch_ring_peers(const TileArgs& a, const void* in, int P, const double2* tw, cudaStream_t st) {
-  constexpr int BOX = L < 256 ? L : 256;
+  constexpr int BOX = L < kBoxRows ? L : kBoxRows;
   EncodeTiledFn enc = encode_fn();
   if (!enc || P < 2 || P > kMaxRanks || L % P) return cudaErrorNotSupported;
   const uint64_t nz2 = (uint64_t)a.nchunk * 8 * 2;
@@ -543,7 +553,7 @@ static cudaError_t launch_ring_peers(const TileArgs& a, const void* in, int P, c
     const cuuint64_t strides[2] = {nz2 * sizeof(double), nz2 * sizeof(double) * a.n_outer};
     const cuuint32_t box[3] = {16, 1, (cuuint32_t)BOX};
     if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(in), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, kL2Promo,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
@@ -555,7 +565,7 @@ static cudaError_t launch_ring_peers(const TileArgs& a, const void* in, int P, c
     const cuuint64_t strides[2] = {nz2 * sizeof(double), nz2 * sizeof(double) * a.n_outer};
     const cuuint32_t box[3] = {16, 1, (cuuint32_t)(nxl < (uint64_t)BOX ? nxl : BOX)};
     if (enc(&pm.m[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.peers[q], dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, kL2Promo,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }

@@ -10,7 +10,7 @@ import io
 import subprocess
 import sys
 
-STEP = ("ring_kernel<512, 2, 2", "zline_kernel<512, 4, 0, double2, 0>", "tile_kernel<512, 0, 0, 0, 0",
+STEP = ("ring_kernel<512, 2, 2", "zline_kernel<512, 4, 0, double2, 0", "tile_kernel<512, 0, 0, 0, 0",
         "tile_kernel<512, 1, 0, 0, 0")
 
 
