@@ -135,7 +135,7 @@ __device__ __forceinline__ void z_observe(const ZArgs& a, const CV* v, int t, ui
   constexpr int T = L / kElems;
   double acc[kObsVals] = {0.0, 0.0, 0.0, 0.0};
   if (active) {
-    const uint32_t x = line / a.ny, y = line - x * a.ny;
+    const uint32_t x = line >> a.lny, y = line & (a.ny - 1u);  // ny is a power of two
     const int mg = a.margin;
     const bool line_edge = (int)x < mg || (int)x >= (int)a.nx - mg || (int)y < mg || (int)y >= (int)a.ny - mg;
     const double xv = __ldg(&a.xs[x]);
@@ -503,6 +503,7 @@ cudaError_t ctap_run_z_last_observe(const ctap_plan* p, void* psi, const double*
   a.xb2 = xb2;
   a.obs_partial = partial;
   a.ny = (uint32_t)p->n[1];
+  a.lny = (uint32_t)ilog2(p->n[1]);
   a.nx = (uint32_t)p->n[0];
   a.margin = margin;
   PhaseArgs& ph = a.ph;

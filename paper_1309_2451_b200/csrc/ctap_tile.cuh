@@ -47,6 +47,7 @@ struct ZArgs {
   const double* xb2;
   double* obs_partial;
   uint32_t ny, nx;     // line = x ny + y
+  uint32_t lny;        // log2(ny)
   int margin;
 };
 
