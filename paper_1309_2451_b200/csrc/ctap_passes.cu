@@ -83,8 +83,12 @@ __device__ __forceinline__ void z_body(const ZArgs& a, CV* v, int t, uint32_t of
     line_fft<L, +1>(v, t, tw, sm, sync);
   } else if constexpr (KIND == T_VFIRST) {  // Vh, then forward
     if (active) {
+      // all eight v_i loads in flight before the first phase
+      double vi[kElems];
 #pragma unroll
-      for (int m = 0; m < kElems; ++m) mul_vphase(v[m], __ldcg(&a.ph.vi[off + t + m * T]), -0.5, a.ph);
+      for (int m = 0; m < kElems; ++m) vi[m] = __ldcg(&a.ph.vi[off + t + m * T]);
+#pragma unroll
+      for (int m = 0; m < kElems; ++m) mul_vphase(v[m], vi[m], -0.5, a.ph);
     }
     line_fft<L, -1>(v, t, tw, sm, sync);
   } else if constexpr (KIND == T_VMID && VTAB) {  // inverse, x exp(-iV dt) table, forward
