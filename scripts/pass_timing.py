@@ -41,8 +41,12 @@ def main():
     total = 0.0
     for name, kind, bpp in passes:
         src, dst = io.get(kind, (psi, psi))
-        for _ in range(3):
-            plan.native.run_pass(kind, src, dst)
+        try:
+            for _ in range(3):
+                plan.native.run_pass(kind, src, dst)
+        except Exception as e:  # diagnostic kinds not built for this size / precision
+            print(f"{name:8s} n/a ({e.__class__.__name__})")
+            continue
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         s.record()
