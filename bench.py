@@ -337,33 +337,30 @@ def run_ours(args):
         xs_d = torch.from_numpy(grid.axis(0)).to(dev)
         xb = (torch.from_numpy(part.xb1).to(dev), torch.from_numpy(part.xb2).to(dev))
 
-        def timed(fn, reps=10):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            a.record(stream)
-            for _ in range(reps):
-                fn()
-            b.record(stream)
-            torch.cuda.synchronize()
-            return a.elapsed_time(b) / reps
-
-        # one-step segments (short enough that clock drift does not swamp the
-        # difference), the three variants interleaved, median of 7 rounds
+        # one-step segments, the three variants interleaved call by call
+        # (A B C A B C ...; clock drift hits neighbours alike), each call
+        # bracketed by its own CUDA events; medians of 25 calls per variant
         plain = lambda: prop.native.advance(flat, 1)
         fusedo = lambda: prop.native.advance_observe(flat, 1, xs_d, *xb, 2)
         separate = lambda: (prop.native.advance(flat, 1), prop.native.observe(flat, xs_d, *xb, 2))
-        for f in (plain, fusedo, separate):
+        variants = (plain, fusedo, separate)
+        for f in variants:
             f()
-        d_f, d_s, t_p = [], [], []
-        for _ in range(9):
-            tp, tf, ts = timed(plain), timed(fusedo), timed(separate)
-            t_p.append(tp)
-            d_f.append(tf - tp)
-            d_s.append(ts - tp)
-        obs_cost = {"segment_steps": 1, "segment_ms": statistics.median(t_p),
-                    "extra_ms_fused": statistics.median(d_f),
-                    "extra_ms_standalone_reduction": statistics.median(d_s),
-                    "method": "CUDA events, 1-step segments x 10, the variants interleaved, median of 9"}
+        evs = [[] for _ in variants]
+        torch.cuda.synchronize()
+        for _ in range(25):
+            for i, f in enumerate(variants):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                f()
+                b.record(stream)
+                evs[i].append((a, b))
+        torch.cuda.synchronize()
+        t_p, t_f, t_s = (statistics.median(a.elapsed_time(b) for a, b in e) for e in evs)
+        obs_cost = {"segment_steps": 1, "segment_ms": t_p,
+                    "extra_ms_fused": t_f - t_p, "extra_ms_standalone_reduction": t_s - t_p,
+                    "method": "CUDA events around each call, 1-step segments, the variants interleaved, "
+                              "median of 25 per variant"}
     dom_name = max(per_pass, key=lambda k: per_pass[k]["ms"])
     dom = per_pass[dom_name]
     peak, peak_kind = _peaks()
