@@ -23,10 +23,11 @@ line; the time is the max over ranks of the CUDA-event time.
 the N-rank path on a one-GPU box; ranks time-share the GPU, so the number is
 not a measurement and says so).
 
---impl reference times the reference's CPU algorithm (oracle/, the numpy +
-scipy.fft port pinned bitwise to the reference; its pooled pointwise
-multiplies as in propagator.py:84-95, scipy.fft workers = all host threads)
-on the same grid.
+--impl reference times the reference's own CPU path on the box's host cores:
+ctapsim (installed unmodified into baseline/_ref) make_plan(threads = all host
+threads) + evolve_real, i.e. the telescoped _advance with its pooled pointwise
+multiplies and scipy.fft workers (propagator.py:84-107) -- or, where
+baseline/_ref is absent, the bitwise-pinned port of it in oracle/.
 """
 
 from __future__ import annotations
@@ -481,61 +482,123 @@ def run_ours(args):
 # ----------------------------------------------------------- CPU oracle arm
 
 def cpu_baseline(grid, v, amp0, mass, steps=3):
-    """The reference algorithm (oracle/, numpy + scipy.fft with the reference's
-    pooled multiplies) on the host cores, on the same workload: make_plan's
-    factors untimed, `steps` split steps timed."""
-    from oracle import split_step as orc
-
-    g = orc.as_grid(grid)
-    t0 = time.perf_counter()
-    f = orc.make_factors(g, v, mass, DT)
-    t_plan = time.perf_counter() - t0
-    amps = np.array(amp0, dtype=np.complex128, copy=True)
-    t0 = time.perf_counter()
-    amps = orc.advance(amps, f, steps)
-    dt = time.perf_counter() - t0
+    """The reference's CPU path on the host cores, on the same workload (the
+    same V and psi0): ctapsim's own make_plan + evolve_real when it is
+    installed in baseline/_ref, else the bitwise-pinned port (oracle/, the
+    reference's _advance with its pooled multiplies).  make_plan untimed,
+    `steps` split steps timed."""
     cores = os.cpu_count()
     n = grid.n
-    return {"value": steps / dt, "unit": "steps/s", "cores": cores, "kind": "port",
-            "sample": f"{steps} telescoped split steps of the full {n[0]}x{n[1]}x{n[2]} grid "
-                      f"(oracle.split_step.advance = reference _advance: scipy.fft workers={cores}, "
-                      f"multiplies chunked over a {cores}-thread pool); make_plan factors built untimed "
-                      f"in {t_plan:.1f} s"}
+    ref = _import_reference()
+    if ref is not None:
+        rprop, rq, _ = ref
+        g = rq.make_grid(*n, tuple(grid.extents), origin=tuple(grid.origin))
+        t0 = time.perf_counter()
+        plan = rprop.make_plan(g, v, mass, DT, threads=cores)
+        t_plan = time.perf_counter() - t0
+        psi = rq.Wavefunction(np.array(amp0, dtype=np.complex128, copy=True), g)
+        t0 = time.perf_counter()
+        rprop.evolve_real(psi, plan, steps)
+        dt = time.perf_counter() - t0
+        kind, what = "reference", (f"ctapsim.propagator.evolve_real (the reference package, baseline/_ref), "
+                                   f"make_plan(threads={cores})")
+    else:
+        from oracle import split_step as orc
+
+        g = orc.as_grid(grid)
+        t0 = time.perf_counter()
+        f = orc.make_factors(g, v, mass, DT)
+        t_plan = time.perf_counter() - t0
+        amps = np.array(amp0, dtype=np.complex128, copy=True)
+        t0 = time.perf_counter()
+        amps = orc.advance(amps, f, steps)
+        dt = time.perf_counter() - t0
+        kind, what = "port", (f"oracle.split_step.advance = reference _advance: scipy.fft workers={cores}, "
+                              f"multiplies chunked over a {cores}-thread pool")
+    return {"value": steps / dt, "unit": "steps/s", "cores": cores, "kind": kind,
+            "sample": f"{steps} telescoped split steps of the full {n[0]}x{n[1]}x{n[2]} grid ({what}); "
+                      f"make_plan built untimed in {t_plan:.1f} s"}
+
+
+def _import_reference():
+    """The reference package itself (ctapsim), installed unmodified into
+    baseline/_ref (`pip install --no-index --no-build-isolation --no-deps
+    --target baseline/_ref <copy of /root/reference/pkg>`; git-ignored, travels
+    to the GPU box with the snapshot).  None if it is not there."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "ctapsim")) and ref not in sys.path:
+        sys.path.insert(0, ref)
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "ctapsim_numba_cache"))
+    try:
+        from ctapsim import constants, propagator, qgrid  # noqa: F401
+
+        return propagator, qgrid, constants
+    except Exception:  # noqa: BLE001 - fall back to the pinned port
+        return None
+
+
+def _timed_steps(advance_k, budget: float, max_steps: int):
+    """One untimed warm step, a 1-step estimate, then as many steps as fit the
+    budget (bounded CPU sample) timed as one call: (steps, seconds)."""
+    advance_k(1)
+    t0 = time.perf_counter()
+    advance_k(1)
+    est = time.perf_counter() - t0
+    k = max(1, min(max_steps, int(budget / max(est, 1e-3))))
+    t0 = time.perf_counter()
+    advance_k(k)
+    return k, time.perf_counter() - t0
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import split_step as orc
-    from paper_1309_2451_b200 import chip
-    from paper_1309_2451_b200.constants import species_mass
-
     n = args.grid
-    grid = _grid(n)
-    g = orc.as_grid(grid)
-    m = species_mass("li6")
-    # V: run_bench's synthetic trap (runner.py:284-288).  The CPU step's cost
-    # does not depend on V's values (runner.py:275-278: numpy multiplies and
-    # pocketfft are data-independent); the paper-chip V our arm uses would
-    # take ~25 min of host Biot-Savart at 512^3 (oracle/potential.c, 16 threads)
-    v = orc.bench_potential(g, m, 5.0)
-    t_pot = 0.0
-    fx, fy, fz = _gaussian_block(grid, slice(None), slice(None))
-    amps = (fx[:, None, None] * fy[None, :, None] * fz[None, None, :]).astype(np.complex128)
-    f = orc.make_factors(g, v, m, DT)
-    for _ in range(max(0, min(args.warmup, 1))):
-        amps = orc.advance(amps, f, 1)
-    t0 = time.perf_counter()
-    amps = orc.advance(amps, f, 1)
-    est = time.perf_counter() - t0
-    budget = 120.0
-    k = max(1, min(args.steps, int(budget / max(est, 1e-3))))
-    t0 = time.perf_counter()
-    amps = orc.advance(amps, f, k)
-    dt = time.perf_counter() - t0
-    val = k / dt
     cores = os.cpu_count()
+    fx, fy, fz = _gaussian_block(_grid(n), slice(None), slice(None))
+    amps = (fx[:, None, None] * fy[None, :, None] * fz[None, None, :]).astype(np.complex128)
+    ref = _import_reference()
+    if ref is not None:
+        # the reference's own public API and stock code path: make_plan with
+        # all host threads, evolve_real (telescoped _advance, pooled multiplies,
+        # scipy.fft workers) -- what runner.run_bench times (runner.py:295-302)
+        rprop, rq, rc = ref
+        m = rc.species_mass("li6")
+        dy = EXTENTS[1] / n[1]
+        g = rq.make_grid(*n, EXTENTS, origin=(-EXTENTS[0] / 2, dy / 2, 0.0))
+        x, y, z = g.meshgrid()
+        c = [g.origin[i] + g.extents[i] / 2 for i in range(3)]
+        om = 2 * np.pi * 5.0
+        v = 0.5 * m * om ** 2 * ((x - c[0]) ** 2 + (y - c[1]) ** 2 + (z - c[2]) ** 2)  # runner.py:284-288
+        del x, y, z
+        plan = rprop.make_plan(g, v, m, DT, threads=cores)
+        psi = rq.Wavefunction(amps, g)
+        k, dt = _timed_steps(lambda s: rprop.evolve_real(psi, plan, s), 120.0, args.steps)
+        kind = "reference"
+        sample = (f"{k} steps of ctapsim.propagator.evolve_real (the reference package itself, installed "
+                  f"unmodified in baseline/_ref) on the full {n[0]}x{n[1]}x{n[2]} grid, make_plan(threads={cores}):"
+                  f" pooled multiplies + scipy.fft workers={cores}")
+    else:
+        from oracle import split_step as orc
+        from paper_1309_2451_b200.constants import species_mass
+
+        g = orc.as_grid(_grid(n))
+        m = species_mass("li6")
+        v = orc.bench_potential(g, m, 5.0)
+        f = orc.make_factors(g, v, m, DT)
+        state = {"a": amps}
+
+        def adv(s):
+            state["a"] = orc.advance(state["a"], f, s)
+
+        k, dt = _timed_steps(adv, 120.0, args.steps)
+        kind = "port"
+        sample = (f"{k} telescoped split steps of the full {n[0]}x{n[1]}x{n[2]} grid on {cores} host threads "
+                  f"(oracle.split_step.advance = reference _advance with its thread-pooled multiplies, "
+                  f"scipy.fft workers={cores}); ctapsim is not installed in baseline/_ref here, so its "
+                  f"bitwise-pinned port runs")
+    val = k / dt
     line = {
         "metric": METRIC, "value": val, "unit": "steps/s", "n_gpus": args.gpus, "steps": k,
         "warmup": args.warmup, "ms_per_step": 1000.0 / val, "higher_is_better": True, "scaling": "strong",
@@ -545,12 +608,7 @@ def run_reference(args):
         "config": _config(n),
         "details": {"decomposition": "host threads"},
         "impl": "reference",
-        "cpu_baseline": {"value": val, "unit": "steps/s", "cores": cores, "kind": "port",
-                         "sample": f"{k} telescoped split steps of the full {n[0]}x{n[1]}x{n[2]} grid on {cores} "
-                                   f"host threads (oracle.split_step.advance = reference _advance with its "
-                                   f"thread-pooled multiplies, scipy.fft workers={cores}); the reference package "
-                                   f"itself is pure Python and not present on the GPU box, so its pinned port "
-                                   f"runs"},
+        "cpu_baseline": {"value": val, "unit": "steps/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
