@@ -238,10 +238,6 @@ def run_ours(args):
             * torch.from_numpy(fz)[None, None, :]).to(torch.complex128)
     psi = amp0.to(dev).contiguous()
 
-    def host_barrier():
-        torch.cuda.synchronize()
-        dist.barrier()
-
     if world == 1:
         prop = _Single(grid, v_local, m)
     elif args.decomp == "pencil":
@@ -249,8 +245,9 @@ def run_ours(args):
         prop = pencil.PencilPropagator(grid, v_local, m, DT, Pr, Pc, rg, cg)
         prop.transport = "nccl"
     else:
-        prop = slab.SlabPropagator(grid, v_local, m, DT, transport=args.transport,
-                                   barrier=host_barrier if args.share_device else None, chunks=args.chunks)
+        # the fused transport's own stream-ordered flag barrier (also with every
+        # rank on one GPU: stream memory operations, no kernel waits on another)
+        prop = slab.SlabPropagator(grid, v_local, m, DT, transport=args.transport, chunks=args.chunks)
         if prop.chunks > 1:
             decomp += f", {prop.chunks} z chunks: chunk c's all-to-all overlaps chunk c+1's pass"
         if getattr(prop, "transport_fallback", None):

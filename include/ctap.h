@@ -191,6 +191,16 @@ CTAP_API int ctap_v_sums(ctap_plan* plan, const void* psi_dev, double* out_dev, 
 CTAP_API int ctap_pass_zchunk(ctap_plan* plan, int32_t kind, const void* in, void* out, int64_t z0, int64_t zn,
                               void* stream);
 
+/* Stream-ordered cross-rank barrier of the fused slab transport: write
+ * `epoch` into slot `rank` of every peer's flag array (peer_flags[q]: rank q's
+ * nranks x uint32 array as mapped in this process), then make `stream` wait
+ * until every peer has written >= epoch into this rank's array (my_flags).
+ * Stream memory operations (cuStreamWriteValue32 / cuStreamWaitValue32): no
+ * kernel spins, no collective.  The flag arrays must start at 0 and epochs
+ * increase by one per barrier. */
+CTAP_API int ctap_flag_barrier(void* const* peer_flags, const void* my_flags, int32_t nranks, int32_t rank,
+                               uint32_t epoch, void* stream);
+
 /* Register, for the fused slab passes, the device addresses (as seen by this
  * process: peer-mapped through ctap_ipc_open, or local) of every rank's
  * buffers: which = 0: the y-slab buffers (nx, ny/P, nz) the y pass writes;
@@ -205,6 +215,7 @@ CTAP_API int ctap_set_peer_buffers(ctap_plan* plan, int32_t which, void* const* 
 CTAP_API int ctap_ipc_handle(void* dev_ptr, void* handle64);
 CTAP_API int ctap_ipc_open(const void* handle64, void** dev_ptr);
 CTAP_API int ctap_ipc_close(void* dev_ptr);
+/* cudaMalloc + zero fill (IPC-exportable; the flag arrays of ctap_flag_barrier rely on the zeros) */
 CTAP_API int ctap_device_alloc(int64_t bytes, void** dev_ptr);
 CTAP_API int ctap_device_free(void* dev_ptr);
 

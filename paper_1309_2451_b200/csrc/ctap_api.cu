@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include "ctap_device.cuh"
@@ -524,9 +525,50 @@ CTAP_API int ctap_ipc_close(void* dev_ptr) {
   return CTAP_OK;
 }
 
+// Stream-ordered flag barrier of the fused slab transport (stream memory
+// operations on peer-mapped flags, no kernel spins and no collective):
+// every rank writes `epoch` into its slot of every peer's flag array after
+// its pass (the write carries a memory barrier, and the pass ends with a
+// system-scope fence), then its stream waits until every peer has written
+// `epoch` into its own array.  The waits are semaphore acquires in the
+// stream front end, the mechanism cross-process event waits use.
+typedef CUresult (*StreamWriteFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*StreamWaitFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+static void* driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return p;
+}
+
+CTAP_API int ctap_flag_barrier(void* const* peer_flags, const void* my_flags, int32_t nranks, int32_t rank,
+                               uint32_t epoch, void* stream) {
+  if (!peer_flags || !my_flags || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(CTAP_EINVAL, "bad flag-barrier arguments");
+  static StreamWriteFn wr = (StreamWriteFn)driver_fn("cuStreamWriteValue32");
+  static StreamWaitFn wt = (StreamWaitFn)driver_fn("cuStreamWaitValue32");
+  if (!wr || !wt) return fail(CTAP_EUNSUPPORTED, "stream memory operations unavailable");
+  CUstream st = (CUstream)stream;
+  for (int q = 0; q < nranks; ++q) {
+    if (q == rank) continue;
+    if (!peer_flags[q]) return fail(CTAP_EINVAL, "peer flag array %d is null", q);
+    const CUresult r = wr(st, (CUdeviceptr)((char*)peer_flags[q] + 4 * rank), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return fail(CTAP_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+  }
+  for (int q = 0; q < nranks; ++q) {
+    if (q == rank) continue;
+    const CUresult r = wt(st, (CUdeviceptr)((const char*)my_flags + 4 * q), epoch, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(CTAP_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  }
+  return CTAP_OK;
+}
+
 CTAP_API int ctap_device_alloc(int64_t bytes, void** dev_ptr) {
   if (!dev_ptr || bytes <= 0) return fail(CTAP_EINVAL, "bad allocation request");
   CUDA_TRY(cudaMalloc(dev_ptr, (size_t)bytes), "ctap_device_alloc");
+  CUDA_TRY(cudaMemset(*dev_ptr, 0, (size_t)bytes), "ctap_device_alloc");  // zeroed (flag arrays rely on it)
   return CTAP_OK;
 }
 

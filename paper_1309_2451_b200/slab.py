@@ -209,7 +209,12 @@ class SlabPropagator:
                  transport: str = "nccl", barrier=None, chunks: int = 1):
         self.grid = as_simgrid(grid)
         self.group = group
-        self._barrier_fn = barrier  # fused transport: default is a 1-float NCCL all-reduce
+        # fused transport's cross-rank barrier after each pass: "flags" (default:
+        # stream-ordered peer flags, ctap_flag_barrier), "nccl" (a 1-float NCCL
+        # all-reduce) or a callable (tests: host barriers)
+        if not (barrier is None or callable(barrier) or barrier in ("flags", "nccl")):
+            raise ValueError(f"unknown barrier {barrier!r}")
+        self._barrier_fn = "flags" if barrier is None else barrier
         P = dist.get_world_size(group) if dist.is_initialized() else 1
         r = dist.get_rank(group) if dist.is_initialized() else 0
         self.layout = SlabLayout(tuple(self.grid.n), P, r)
@@ -258,24 +263,28 @@ class SlabPropagator:
         try:
             self.yslab = DeviceBuffer(nbytes)
             self.peer = DeviceBuffer(nbytes)
-            mine = (self.yslab.ipc_handle(), self.peer.ipc_handle())
+            self.flags = DeviceBuffer(4 * self.layout.P)  # zeroed: the barrier's epoch slots
+            mine = (self.yslab.ipc_handle(), self.peer.ipc_handle(), self.flags.ipc_handle())
         except Exception as e:  # noqa: BLE001 - reported to every rank below
             err = f"rank {self.layout.rank}: {e}"
         handles = [None] * self.layout.P
         dist.all_gather_object(handles, mine, group=self.group)
         self._opened = []
         tabs = ([], [])
+        self._peer_flags = []
         if err is None and all(h is not None for h in handles):
             try:
-                for q, (hy, hp) in enumerate(handles):
+                for q, (hy, hp, hf) in enumerate(handles):
                     if q == self.layout.rank:
                         tabs[0].append(self.yslab.ptr)
                         tabs[1].append(self.peer.ptr)
+                        self._peer_flags.append(self.flags.ptr)
                     else:
-                        py, pp = open_ipc(hy), open_ipc(hp)
-                        self._opened += [py, pp]
+                        py, pp, pf = open_ipc(hy), open_ipc(hp), open_ipc(hf)
+                        self._opened += [py, pp, pf]
                         tabs[0].append(py)
                         tabs[1].append(pp)
+                        self._peer_flags.append(pf)
                 self.native.set_peer_buffers(0, tabs[0])
                 self.native.set_peer_buffers(1, tabs[1])
             except Exception as e:  # noqa: BLE001
@@ -294,9 +303,11 @@ class SlabPropagator:
             for ptr in self._opened:
                 _lib.load().ctap_ipc_close(ctypes.c_void_p(ptr))
             self._opened = []
-            self.yslab = self.peer = None
+            self.yslab = self.peer = self.flags = None
             return False
         self._flag = torch.zeros(1, dtype=torch.float32, device=self.v_local.device)
+        self._epoch = 0
+        self._peer_flag_arr = (ctypes.c_void_p * self.layout.P)(*self._peer_flags)
         return True
 
     def close(self):
@@ -314,16 +325,20 @@ class SlabPropagator:
             _lib.load().ctap_ipc_close(ctypes.c_void_p(ptr))
         self._opened = []
         dist.barrier(group=self.group)  # every rank unmapped before the owners free
-        self.yslab = self.peer = None
+        self.yslab = self.peer = self.flags = None
         self.transport = "closed"
 
     def _barrier(self):
         # stream-ordered: every rank's preceding pass (and its system fence)
         # completes before any rank's next pass starts
-        if self._barrier_fn is not None:
-            self._barrier_fn()
-        else:
+        if self._barrier_fn == "flags":
+            self._epoch += 1
+            _lib.call("ctap_flag_barrier", self._peer_flag_arr, ctypes.c_void_p(self.flags.ptr), self.layout.P,
+                      self.layout.rank, self._epoch, _device.stream_handle())
+        elif self._barrier_fn == "nccl":
             dist.all_reduce(self._flag, group=self.group)
+        else:
+            self._barrier_fn()
 
     def _a2a(self, src: torch.Tensor, dst: torch.Tensor):
         if self.layout.P == 1:

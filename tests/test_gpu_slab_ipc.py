@@ -40,7 +40,7 @@ def _case(n=(32, 16, 32)):
     return grid, v, a0, m
 
 
-def _worker(rank, world, port, steps, out, n):
+def _worker(rank, world, port, steps, out, n, barrier_mode="host"):
     here = os.path.dirname(os.path.abspath(__file__))
     for p in (here, os.path.dirname(here)):
         if p not in sys.path:
@@ -59,7 +59,9 @@ def _worker(rank, world, port, steps, out, n):
             dist.barrier()
 
         prop = slab.SlabPropagator(grid, torch.from_numpy(np.ascontiguousarray(v[lay.x_slice])).cuda(), m, 1e-6,
-                                   phase_tables=0, transport="fused", barrier=barrier)
+                                   phase_tables=0, transport="fused",
+                                   barrier=barrier if barrier_mode == "host" else barrier_mode)
+        assert prop.transport == "fused", prop.transport_fallback
         psi = torch.from_numpy(np.ascontiguousarray(a0[lay.x_slice])).cuda()
         prop.advance(psi, steps)
         torch.cuda.synchronize()
@@ -71,14 +73,18 @@ def _worker(rank, world, port, steps, out, n):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, (32, 16, 32)), (2, (512, 8, 16))])
-def test_fused_ipc_two_processes_bitwise(tmp_path, world, n):
+@pytest.mark.parametrize("world,n,barrier_mode", [(2, (32, 16, 32), "host"), (2, (512, 8, 16), "host"),
+                                                  (2, (32, 16, 32), "flags"), (2, (512, 8, 16), "flags")])
+def test_fused_ipc_two_processes_bitwise(tmp_path, world, n, barrier_mode):
     """n = (512, ...) runs the x pass through the warp-per-line ring, whose TMA
-    stores then target the other process's IPC-mapped buffer."""
+    stores then target the other process's IPC-mapped buffer.  barrier_mode
+    "flags": the transport's own stream-ordered barrier (ctap_flag_barrier:
+    peer-mapped epoch flags written and awaited by stream memory operations,
+    no kernel spins), the default on a multi-GPU box."""
     from paper_1309_2451_b200 import propagator, qgrid
 
     out = str(tmp_path / "psi")
-    mp.spawn(_worker, args=(world, _port(), 5, out, n), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _port(), 5, out, n, barrier_mode), nprocs=world, join=True)
     got = np.concatenate([np.load(f"{out}.{r}.npy") for r in range(world)])
     grid, v, a0, m = _case(n)
     psi = qgrid.Wavefunction(a0.copy(), grid)
