@@ -12,7 +12,7 @@ import torch
 from conftest import load_golden, oracle_grid, product_grid
 from oracle import potential as opot
 from oracle import split_step as orc
-from paper_1309_2451_b200 import magfield, observables, propagator, qgrid
+from paper_1309_2451_b200 import _lib, magfield, observables, propagator, qgrid
 from paper_1309_2451_b200.constants import species_mass
 
 pytestmark = pytest.mark.gpu
@@ -356,3 +356,32 @@ def test_1024_line_tiles_bitwise(tmp_path):
                        env=dict(os.environ, CTAP_W1024=w, PYTHONPATH=root))
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("n", [(16, 16, 64), (8, 8, 512), (8, 8, 1024)])
+def test_two_stage_z_fft_option(monkeypatch, n):
+    """CTAP_Z2=1 (ctap_zline2.cu: the two-stage 32 x L/32 z transform, opt-in
+    because it measured slower at 512^3) against the oracle and the default
+    radix-8 z passes."""
+    grid = qgrid.make_grid(*n, (20e-6, 4e-6, 250e-6), origin=(-10e-6, 4e-6 / n[1] / 2, 0.0))
+    rng = np.random.default_rng(17)
+    x, y, z = grid.meshgrid()
+    v = 0.5 * M * ((2 * np.pi * 2e3) ** 2 * x ** 2 + (2 * np.pi * 20.0) ** 2 * (z - 125e-6) ** 2) + 1e-28
+    a0 = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    og = orc.as_grid(grid)
+    ref = orc.advance(a0.copy(), orc.make_factors(og, v, M, 1e-6), 10)
+
+    def run(z2):
+        monkeypatch.setenv("CTAP_Z2", z2)
+        psi = qgrid.Wavefunction(a0.copy(), grid)
+        psi, _ = propagator.evolve_real(psi, propagator.make_plan(grid, v, M, 1e-6), 10)
+        return psi.amplitudes
+
+    got2, got1 = run("1"), run("0")
+    assert rel_l2(got2, ref) <= REL_L2
+    assert rel_l2(got2, got1) <= 1e-13
+    d = torch.from_numpy(a0.copy()).cuda()
+    monkeypatch.setenv("CTAP_Z2", "1")
+    plan = propagator.make_plan(grid, v, M, 1e-6).native
+    plan.run_pass(_lib.PASS_Z_FWD, d, d)
+    assert rel_l2(d.cpu().numpy(), np.fft.fft(a0, axis=2)) <= 1e-14
