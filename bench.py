@@ -247,7 +247,10 @@ def run_ours(args):
     else:
         # the fused transport's own stream-ordered flag barrier (also with every
         # rank on one GPU: stream memory operations, no kernel waits on another)
-        prop = slab.SlabPropagator(grid, v_local, m, DT, transport=args.transport, chunks=args.chunks)
+        prop = slab.SlabPropagator(grid, v_local, m, DT, transport=args.transport, chunks=args.chunks,
+                                   graphs=args.transport == "fused")
+        if prop.transport == "fused":
+            decomp += ", one CUDA graph per segment (passes + flag barriers)"
         if prop.chunks > 1:
             decomp += f", {prop.chunks} z chunks: chunk c's all-to-all overlaps chunk c+1's pass"
         if getattr(prop, "transport_fallback", None):

@@ -197,7 +197,9 @@ CTAP_API int ctap_pass_zchunk(ctap_plan* plan, int32_t kind, const void* in, voi
  * until every peer has written >= epoch into this rank's array (my_flags).
  * Stream memory operations (cuStreamWriteValue32 / cuStreamWaitValue32): no
  * kernel spins, no collective.  The flag arrays must start at 0 and epochs
- * increase by one per barrier. */
+ * increase by one per barrier; epoch 0 clears this rank's array instead
+ * (stream-ordered), e.g. before replaying a captured segment that reuses
+ * epochs 1, 2, ... (every rank must have cleared before any rank writes). */
 CTAP_API int ctap_flag_barrier(void* const* peer_flags, const void* my_flags, int32_t nranks, int32_t rank,
                                uint32_t epoch, void* stream);
 

@@ -545,8 +545,13 @@ static void* driver_fn(const char* name) {
 
 CTAP_API int ctap_flag_barrier(void* const* peer_flags, const void* my_flags, int32_t nranks, int32_t rank,
                                uint32_t epoch, void* stream) {
-  if (!peer_flags || !my_flags || nranks < 1 || rank < 0 || rank >= nranks)
-    return fail(CTAP_EINVAL, "bad flag-barrier arguments");
+  if (!my_flags || nranks < 1 || rank < 0 || rank >= nranks) return fail(CTAP_EINVAL, "bad flag-barrier arguments");
+  if (epoch == 0) {  // clear this rank's array (stream-ordered) before a new epoch sequence
+    CUDA_TRY(cudaMemsetAsync(const_cast<void*>(my_flags), 0, 4 * (size_t)nranks, (cudaStream_t)stream),
+             "ctap_flag_barrier");
+    return CTAP_OK;
+  }
+  if (!peer_flags) return fail(CTAP_EINVAL, "bad flag-barrier arguments");
   static StreamWriteFn wr = (StreamWriteFn)driver_fn("cuStreamWriteValue32");
   static StreamWaitFn wt = (StreamWaitFn)driver_fn("cuStreamWaitValue32");
   if (!wr || !wt) return fail(CTAP_EUNSUPPORTED, "stream memory operations unavailable");

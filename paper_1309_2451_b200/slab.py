@@ -206,9 +206,10 @@ class SlabPropagator:
 
     def __init__(self, grid, v_local, mass: float, dt: float, group=None, mode: str = REAL_TIME,
                  v_shift: float = 0.0, phase_tables: int | None = None, precision: str = "complex128",
-                 transport: str = "nccl", barrier=None, chunks: int = 1):
+                 transport: str = "nccl", barrier=None, chunks: int = 1, graphs: bool = False):
         self.grid = as_simgrid(grid)
         self.group = group
+        self.graphs = bool(graphs)  # fused transport: one CUDA graph per segment
         # fused transport's cross-rank barrier after each pass: "flags" (default:
         # stream-ordered peer flags, ctap_flag_barrier), "nccl" (a 1-float NCCL
         # all-reduce) or a callable (tests: host barriers)
@@ -356,12 +357,10 @@ class SlabPropagator:
         if self.transport == "closed":
             raise RuntimeError("SlabPropagator was closed")
         if self.transport == "fused":
-            addr = {"psi": psi_local.data_ptr(), "yslab": self.yslab.ptr, "peer": self.peer.ptr}
-            for op in segment_schedule_fused(n_steps):
-                if op[0] == "pass":
-                    self.native.run_pass_ptr(op[1], addr[op[2]], addr[op[3]])
-                else:
-                    self._barrier()
+            if self.graphs and self._barrier_fn == "flags":
+                self._advance_fused_graph(psi_local, n_steps)
+                return
+            self._fused_ops(psi_local, n_steps)
             return
         if self.chunks > 1:
             self._advance_chunked(psi_local, n_steps)
@@ -373,6 +372,33 @@ class SlabPropagator:
                 self.native.run_pass(kind, bufs[src], bufs[dst])
             else:
                 self._a2a(bufs[op[1]], bufs[op[2]])
+
+    def _fused_ops(self, psi_local: torch.Tensor, n_steps: int):
+        addr = {"psi": psi_local.data_ptr(), "yslab": self.yslab.ptr, "peer": self.peer.ptr}
+        for op in segment_schedule_fused(n_steps):
+            if op[0] == "pass":
+                self.native.run_pass_ptr(op[1], addr[op[2]], addr[op[3]])
+            else:
+                self._barrier()
+
+    def _advance_fused_graph(self, psi_local: torch.Tensor, n_steps: int):
+        """The fused segment as ONE CUDA graph per rank: its passes and flag
+        barriers (stream memory operations) captured once per (psi, n) and
+        replayed.  A replay reuses the captured epochs 1..2n, so every rank
+        clears its flag array and passes a host barrier first (one per
+        segment, not per step)."""
+        key = (psi_local.data_ptr(), int(n_steps))
+        if getattr(self, "_graph_key", None) != key:
+            g = torch.cuda.CUDAGraph()
+            self._epoch = 0
+            with torch.cuda.graph(g):
+                self._fused_ops(psi_local, n_steps)
+            self._graph, self._graph_key = g, key
+        _lib.call("ctap_flag_barrier", None, ctypes.c_void_p(self.flags.ptr), self.layout.P, self.layout.rank, 0,
+                  _device.stream_handle())
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)
+        self._graph.replay()
 
     def _advance_chunked(self, psi_local: torch.Tensor, n_steps: int):
         """segment_schedule_chunked on two streams: passes on the current

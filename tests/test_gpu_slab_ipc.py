@@ -58,12 +58,15 @@ def _worker(rank, world, port, steps, out, n, barrier_mode="host"):
             torch.cuda.synchronize()
             dist.barrier()
 
+        graphs = barrier_mode == "flags_graph"
         prop = slab.SlabPropagator(grid, torch.from_numpy(np.ascontiguousarray(v[lay.x_slice])).cuda(), m, 1e-6,
-                                   phase_tables=0, transport="fused",
-                                   barrier=barrier if barrier_mode == "host" else barrier_mode)
+                                   phase_tables=0, transport="fused", graphs=graphs,
+                                   barrier=barrier if barrier_mode == "host" else "flags")
         assert prop.transport == "fused", prop.transport_fallback
         psi = torch.from_numpy(np.ascontiguousarray(a0[lay.x_slice])).cuda()
         prop.advance(psi, steps)
+        if graphs:  # a second segment replays the captured graph
+            prop.advance(psi, steps)
         torch.cuda.synchronize()
         np.save(f"{out}.{rank}.npy", psi.cpu().numpy())
         sums = prop.observe(psi, np.full(grid.n[2], -3.5e-6), np.full(grid.n[2], 3.5e-6), 2)
@@ -74,7 +77,8 @@ def _worker(rank, world, port, steps, out, n, barrier_mode="host"):
 
 
 @pytest.mark.parametrize("world,n,barrier_mode", [(2, (32, 16, 32), "host"), (2, (512, 8, 16), "host"),
-                                                  (2, (32, 16, 32), "flags"), (2, (512, 8, 16), "flags")])
+                                                  (2, (32, 16, 32), "flags"), (2, (512, 8, 16), "flags"),
+                                                  (2, (32, 16, 32), "flags_graph"), (2, (512, 8, 16), "flags_graph")])
 def test_fused_ipc_two_processes_bitwise(tmp_path, world, n, barrier_mode):
     """n = (512, ...) runs the x pass through the warp-per-line ring, whose TMA
     stores then target the other process's IPC-mapped buffer.  barrier_mode
@@ -88,7 +92,10 @@ def test_fused_ipc_two_processes_bitwise(tmp_path, world, n, barrier_mode):
     got = np.concatenate([np.load(f"{out}.{r}.npy") for r in range(world)])
     grid, v, a0, m = _case(n)
     psi = qgrid.Wavefunction(a0.copy(), grid)
-    psi, _ = propagator.evolve_real(psi, propagator.make_plan(grid, v, m, 1e-6, phase_tables=0), 5)
+    plan = propagator.make_plan(grid, v, m, 1e-6, phase_tables=0)
+    psi, _ = propagator.evolve_real(psi, plan, 5)
+    if barrier_mode == "flags_graph":  # two segments of 5 (the second a graph replay)
+        psi, _ = propagator.evolve_real(psi, plan, 5)
     assert np.array_equal(got, psi.amplitudes)
     s0, s1 = (np.load(f"{out}.{r}.sums.npy") for r in range(world))
     assert np.array_equal(s0, s1)  # rank-ordered combination: identical on every rank
