@@ -499,7 +499,16 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-static int sm_count() { return ctap_sm_count(); }
+// CTAs of the persistent ring: one per SM, or CTAP_RING_SMS (experiments:
+// leave SMs to a concurrently running pass)
+static int sm_count() {
+  static const int cap = [] {
+    const char* e = getenv("CTAP_RING_SMS");
+    return e ? atoi(e) : 0;
+  }();
+  const int n = ctap_sm_count();
+  return cap > 0 && cap < n ? cap : n;
+}
 
 // AXIS 2: x lines of an (L, n_outer, nz) array; AXIS 1: y lines of an
 // (n_outer, L, nz) array (nz = 8 * a.nchunk)
