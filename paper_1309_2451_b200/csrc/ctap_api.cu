@@ -562,9 +562,15 @@ CTAP_API int ctap_flag_barrier(void* const* peer_flags, const void* my_flags, in
     const CUresult r = wr(st, (CUdeviceptr)((char*)peer_flags[q] + 4 * rank), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
     if (r != CUDA_SUCCESS) return fail(CTAP_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
   }
+  // where the device supports it, the wait also flushes outstanding remote
+  // writes, so peer stores ordered before the flag are visible to the next pass
+  int dev = 0, can_flush = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&can_flush, cudaDevAttrCanFlushRemoteWrites, dev);
+  const unsigned wflags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
   for (int q = 0; q < nranks; ++q) {
     if (q == rank) continue;
-    const CUresult r = wt(st, (CUdeviceptr)((const char*)my_flags + 4 * q), epoch, CU_STREAM_WAIT_VALUE_GEQ);
+    const CUresult r = wt(st, (CUdeviceptr)((const char*)my_flags + 4 * q), epoch, wflags);
     if (r != CUDA_SUCCESS) return fail(CTAP_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
   }
   return CTAP_OK;
