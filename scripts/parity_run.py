@@ -9,6 +9,7 @@ cfg2   128x128x256 scaled-chip CTAP (configs/scaled.cfg with n_y = 128),
 cfg3   256^3 paper-chip CTAP, 1000 steps / 100
 cfg4   512^3 paper-chip CTAP, 100 steps / 50
 cfg3c64 / cfg4c64  the same in complex64 mode, gate 1e-4 against the oracle
+cfg5   1024x1024x512 harmonic trap, 5 steps (one GPU vs the oracle, ~50 GB host RAM)
 
 The cases are tests/baseline_cases.py's (shared with the driver-run
 tests/test_gpu_baseline_configs.py, which runs them at bounded step counts).
@@ -36,6 +37,7 @@ CASES = {
     "cfg4": lambda: (bc.cfg4(every=8), 100, "complex128"),
     "cfg3c64": lambda: (bc.cfg3(every=8), 1000, "complex64"),
     "cfg4c64": lambda: (bc.cfg4(every=8), 100, "complex64"),
+    "cfg5": lambda: (bc.cfg5(), 5, "complex128"),
 }
 
 

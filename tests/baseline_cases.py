@@ -98,6 +98,16 @@ def cfg4(every=16):
                 v_check=check)
 
 
+def cfg5():
+    """BASELINE config 5 grid (1024 x 1024 x 512) with run_bench's harmonic
+    trap ("harmonic synthetic"), a Gaussian packet; ~50 GB of
+    host RAM on the oracle side, so a few steps only."""
+    og, grid = _grid((1024, 1024, 512), 1000e-6)
+    v = orc.bench_potential(og, M, 5.0)
+    a0 = orc.gaussian_packet(og, (-2e-6, 2e-6, 500e-6), (1e-6, 0.3e-6, 40e-6))
+    return dict(name="cfg5 1024x1024x512 harmonic", grid=grid, og=og, v=v, a0=a0, stride=5, half_gap=3.5e-6)
+
+
 def run_case(case, steps: int, stride: int | None = None, precision: str = "complex128") -> dict:
     """GPU (public API, host psi in / out) then the oracle on the same inputs."""
     grid, og, v, a0 = case["grid"], case["og"], case["v"], case["a0"]
