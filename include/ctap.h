@@ -179,6 +179,12 @@ CTAP_API int ctap_density_xz(ctap_plan* plan, const void* psi_dev, double* out_d
  * ctap_v_sums: on position space, out_dev[2] = [ sum V |psi|^2, sum |psi|^2 ]. */
 CTAP_API int ctap_k2_sums(ctap_plan* plan, const void* phi_dev, double* out_dev, void* stream);
 CTAP_API int ctap_v_sums(ctap_plan* plan, const void* psi_dev, double* out_dev, void* stream);
+/* The same sums against a caller's potential V (device, the plan's block
+ * shape): potential_expectation(psi, V) (propagator.py:188-190) on any plan
+ * of the grid, e.g. a cached potential-free one, without building a plan
+ * around V. */
+CTAP_API int ctap_v_sums_with(ctap_plan* plan, const void* psi_dev, const double* v_dev, double* out_dev,
+                              void* stream);
 
 /* The slab kinetic block by z chunks (overlapped NCCL transport): kinds
  * CTAP_PASS_Y_FWD_TO_PEER (psi columns [z0, z0+zn) -> send chunk),

@@ -36,7 +36,7 @@ PASS_PZ_FIRST, PASS_PZ_MID, PASS_PZ_LAST, PASS_PY_FWD, PASS_PY_INV, PASS_PX_KIN 
 # every symbol include/ctap.h declares
 EXPORTS = (
     "ctap_plan_create", "ctap_plan_destroy", "ctap_advance", "ctap_advance_observe", "ctap_pass", "ctap_pass_zchunk", "ctap_observe",
-    "ctap_density_xz", "ctap_k2_sums", "ctap_v_sums", "ctap_phase_field", "ctap_scale",
+    "ctap_density_xz", "ctap_k2_sums", "ctap_v_sums", "ctap_v_sums_with", "ctap_phase_field", "ctap_scale",
     "ctap_fft3d", "ctap_potential", "ctap_last_error", "ctap_version",
     "ctap_set_peer_buffers", "ctap_ipc_handle", "ctap_ipc_open", "ctap_ipc_close",
     "ctap_device_alloc", "ctap_device_free", "ctap_slice_minima", "ctap_flag_barrier",
@@ -88,6 +88,7 @@ def load():
         "ctap_density_xz": [p, p, p, p],
         "ctap_k2_sums": [p, p, p, p],
         "ctap_v_sums": [p, p, p, p],
+        "ctap_v_sums_with": [p, p, p, p, p],
         "ctap_phase_field": [p, i32, p, p],
         "ctap_scale": [p, p, d, p],
         "ctap_fft3d": [p, p, i32, p],

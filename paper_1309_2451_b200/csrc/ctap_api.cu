@@ -31,7 +31,7 @@ struct Range {
 cudaError_t ctap_run_observe(const ctap_plan* p, const void* psi, const double* xs, const double* xb1,
                              const double* xb2, int margin, double* out, cudaStream_t st);
 cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, cudaStream_t st);
-cudaError_t ctap_run_v_sums(const ctap_plan* p, const void* psi, double* out, cudaStream_t st);
+cudaError_t ctap_run_v_sums(const ctap_plan* p, const void* psi, const double* V, double* out, cudaStream_t st);
 cudaError_t ctap_run_density_xz(const ctap_plan* p, const void* psi, double* out, cudaStream_t st);
 cudaError_t ctap_run_scale(const ctap_plan* p, void* psi, double d, cudaStream_t st);
 cudaError_t ctap_run_potential(const double* xs, int64_t nx, const double* ys, int64_t ny, const double* zs,
@@ -482,7 +482,13 @@ CTAP_API int ctap_k2_sums(ctap_plan* p, const void* phi, double* out, void* stre
 CTAP_API int ctap_v_sums(ctap_plan* p, const void* psi, double* out, void* stream) {
   if (!p || !psi || !out) return fail(CTAP_EINVAL, "null argument");
   if (!p->v_dev) return fail(CTAP_EINVAL, "plan has no potential");
-  CUDA_TRY(ctap_run_v_sums(p, psi, out, (cudaStream_t)stream), "ctap_v_sums");
+  CUDA_TRY(ctap_run_v_sums(p, psi, nullptr, out, (cudaStream_t)stream), "ctap_v_sums");
+  return CTAP_OK;
+}
+
+CTAP_API int ctap_v_sums_with(ctap_plan* p, const void* psi, const double* v_dev, double* out, void* stream) {
+  if (!p || !psi || !v_dev || !out) return fail(CTAP_EINVAL, "null argument");
+  CUDA_TRY(ctap_run_v_sums(p, psi, v_dev, out, (cudaStream_t)stream), "ctap_v_sums_with");
   return CTAP_OK;
 }
 

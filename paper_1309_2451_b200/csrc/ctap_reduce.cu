@@ -249,15 +249,17 @@ cudaError_t ctap_run_k2_sums(const ctap_plan* p, const void* phi, double* out, c
 }
 
 template <typename CV>
-static cudaError_t v_t(const ctap_plan* p, const void* psi, double* out, cudaStream_t st) {
+static cudaError_t v_t(const ctap_plan* p, const void* psi, const double* V, double* out, cudaStream_t st) {
   VF<CV> f;
   f.psi = (const CV*)psi;
-  f.V = p->v_dev;
+  f.V = V;
   return run_reduce<2>(p, f, p->nx_local * p->ny_pos * p->n[2], out, st);
 }
 
-cudaError_t ctap_run_v_sums(const ctap_plan* p, const void* psi, double* out, cudaStream_t st) {
-  return p->dtype == CTAP_C64 ? v_t<float2>(p, psi, out, st) : v_t<double2>(p, psi, out, st);
+// V = nullptr: the plan's own potential
+cudaError_t ctap_run_v_sums(const ctap_plan* p, const void* psi, const double* V, double* out, cudaStream_t st) {
+  if (!V) V = p->v_dev;
+  return p->dtype == CTAP_C64 ? v_t<float2>(p, psi, V, out, st) : v_t<double2>(p, psi, V, out, st);
 }
 
 cudaError_t ctap_run_density_xz(const ctap_plan* p, const void* psi, double* out, cudaStream_t st) {

@@ -17,6 +17,7 @@ four fused axis passes per step.
 from __future__ import annotations
 
 import ctypes
+from collections import OrderedDict
 import os
 import sys
 import time as _time
@@ -165,11 +166,12 @@ class NativePlan:
         return out
 
 
-_AUX = {}
+_AUX = OrderedDict()
+_AUX_MAX = 8  # potential-free plans kept (least recently used evicted)
 
 
 def _aux_plan(grid, dtype=torch.complex128) -> NativePlan:
-    """A potential-free plan for FFTs and reductions on `grid` (cached)."""
+    """A potential-free plan for FFTs and reductions on `grid` (LRU-cached)."""
     key = (grid_key(grid), torch.cuda.current_device() if torch.cuda.is_available() else -1, dtype)
     p = _AUX.get(key)
     if p is None:
@@ -178,6 +180,10 @@ def _aux_plan(grid, dtype=torch.complex128) -> NativePlan:
         prec = "complex64" if dtype == torch.complex64 else "complex128"
         p = NativePlan(grid, None, species_mass("li6"), 1e-6, precision=prec)
         _AUX[key] = p
+        while len(_AUX) > _AUX_MAX:
+            _AUX.popitem(last=False)
+    else:
+        _AUX.move_to_end(key)
     return p
 
 
@@ -419,9 +425,15 @@ def kinetic_expectation(psi, mass: float, workers: int = 1) -> float:
 
 def _potential_from(w: Wavefunction, potential) -> float:
     v_dev = _device.to_device_f64(potential)
+    if tuple(v_dev.shape) != tuple(w.grid.n):
+        raise ValueError(f"potential shape {tuple(v_dev.shape)} does not match the grid {tuple(w.grid.n)}")
     d = w.device_amplitudes(None)
-    plan = NativePlan(w.grid, v_dev, 1.0, 1.0, precision="complex64" if d.dtype == torch.complex64 else "complex128")
-    s = plan.v_sums(d).tolist()
+    # the cached potential-free plan of the grid, V passed to the reduction
+    # (no per-call plan with its v_i buffer and device synchronize)
+    plan = _aux_plan(w.grid, d.dtype)
+    out = torch.empty(2, dtype=torch.float64, device=d.device)
+    _lib.call("ctap_v_sums_with", plan.handle, d.data_ptr(), v_dev.data_ptr(), out.data_ptr(), _device.stream_handle())
+    s = out.tolist()
     return s[0] / s[1]
 
 
