@@ -104,15 +104,20 @@ __device__ __forceinline__ void z_body(const ZArgs& a, CV* v, int t, uint32_t of
     line_fft<L, -1>(v, t, tw, sm, sync);
   } else {  // T_VMID: inverse, V, forward; T_VLAST: inverse, Vh
     double vi[kElems];
-#ifndef CTAP_Z_VLATE
-#pragma unroll
-    for (int m = 0; m < kElems; ++m) vi[m] = active ? __ldcg(&a.ph.vi[off + t + m * T]) : 0.0;
+    // v_i loaded before the inverse transform (its latency hides behind it),
+    // all but the last: holding all eight across the transform made ptxas
+    // spill at the 80-register budget (45 spill instructions vs 23), and the
+    // spill traffic shares the L1 pipe this kernel is bound by --
+    // [z^-1 V z] 1.08 -> 1.02 ms at 512^3 (8 / 7 / 6 / 5 early: 1.08 / 1.02 /
+    // 1.02 / 1.09; same-box A/B, bitwise identical results)
+#ifndef CTAP_Z_VEARLY
+#define CTAP_Z_VEARLY 7
 #endif
+#pragma unroll
+    for (int m = 0; m < CTAP_Z_VEARLY; ++m) vi[m] = active ? __ldcg(&a.ph.vi[off + t + m * T]) : 0.0;
     line_fft<L, +1>(v, t, tw, sm, sync);
-#ifdef CTAP_Z_VLATE
 #pragma unroll
-    for (int m = 0; m < kElems; ++m) vi[m] = active ? __ldcg(&a.ph.vi[off + t + m * T]) : 0.0;
-#endif
+    for (int m = CTAP_Z_VEARLY; m < kElems; ++m) vi[m] = active ? __ldcg(&a.ph.vi[off + t + m * T]) : 0.0;
 #pragma unroll
     for (int m = 0; m < kElems; ++m) mul_vphase(v[m], vi[m], KIND == T_VMID ? -1.0 : -0.5, a.ph);
     if constexpr (KIND == T_VMID) line_fft<L, -1>(v, t, tw, sm, sync);
