@@ -259,6 +259,7 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
   cudaFree(p->twiddles32);
   cudaFree(p->sctab);
   cudaFree(p->obs_partial);
+  cudaFree(p->obs_mask);
   cudaFree(p->red_partial);
   cudaFree(p->vi_dev);
   cudaFree(p->expv_dev);
@@ -436,7 +437,10 @@ CTAP_API int ctap_advance_observe(ctap_plan* p, void* psi, int64_t n, const doub
   const int rc = ctap_advance(p, psi, n, stream);
   p->skip_last = 0;
   if (rc != CTAP_OK) return rc;
-  CUDA_TRY(ctap_run_z_last_observe(p, psi, xs, xb1, xb2, margin, p->obs_partial, st), "ctap_advance_observe");
+  if (xb1 && !p->obs_mask)
+    CUDA_TRY(cudaMalloc((void**)&p->obs_mask, sizeof(uint16_t) * ctap_obs_mask_entries(p)), "ctap_advance_observe");
+  CUDA_TRY(ctap_run_z_last_observe(p, psi, xs, xb1, xb2, margin, p->obs_partial, p->obs_mask, st),
+           "ctap_advance_observe");
   CUDA_TRY(ctap_run_finalize5(p, p->obs_partial, ctap_z_blocks(p), out, xb1 != nullptr, st), "ctap_advance_observe");
   return CTAP_OK;
 }

@@ -83,6 +83,7 @@ struct ctap_plan {
   void* peer_p[16];        // and peer-major buffer (peer-mapped device addresses)
   double* red_partial;     // reduction scratch
   double* obs_partial;     // per-block partials of the fused segment-end observer sums (lazy)
+  uint16_t* obs_mask;      // guide-partition bits of the fused observer pass (lazy)
   int skip_last;           // ctap_advance_observe: ctap_advance stops before the segment-end pass
   // CUDA graph of M interior steps (launch-bound small grids), captured on a
   // private stream for one psi pointer and replayed on the caller's stream
@@ -107,8 +108,10 @@ struct ZArgs;
 int64_t ctap_z_blocks(const ctap_plan* p);
 cudaError_t ctap_run_pass_chunk(const ctap_plan* p, int kind, const void* in, void* out, int64_t z0, int64_t zn,
                                 cudaStream_t st);
+size_t ctap_obs_mask_entries(const ctap_plan* p);
 cudaError_t ctap_run_z_last_observe(const ctap_plan* p, void* psi, const double* xs, const double* xb1,
-                                    const double* xb2, int margin, double* partial, cudaStream_t st);
+                                    const double* xb2, int margin, double* partial, uint16_t* mask,
+                                    cudaStream_t st);
 cudaError_t ctap_run_finalize5(const ctap_plan* p, const double* partial, int64_t npartials, double* out,
                                int part, cudaStream_t st);
 cudaError_t ctap_run_z2(const ctap_plan* p, int tkind, bool vtab, int ch, const ctap::ZArgs& a, cudaStream_t st);

@@ -147,16 +147,16 @@ __device__ __forceinline__ void z_observe(const ZArgs& a, const CV* v, int t, ui
     const uint32_t x = line >> a.lny, y = line & (a.ny - 1u);  // ny is a power of two
     const int mg = a.margin;
     const bool line_edge = (int)x < mg || (int)x >= (int)a.nx - mg || (int)y < mg || (int)y >= (int)a.ny - mg;
-    const double xv = __ldg(&a.xs[x]);
-    const bool part = a.xb1 != nullptr;
+    const bool part = a.obs_mask != nullptr;
+    const uint32_t mk = part ? __ldg(&a.obs_mask[x * T + t]) : 0u;
 #pragma unroll
     for (int m = 0; m < kElems; ++m) {
       const int z = t + m * T;
       const double rho = (double)v[m].x * v[m].x + (double)v[m].y * v[m].y;
       acc[0] += rho;
       if (part) {
-        if (xv < __ldg(&a.xb1[z])) acc[1] += rho;
-        if (xv >= __ldg(&a.xb2[z])) acc[2] += rho;
+        if (mk >> m & 1u) acc[1] += rho;
+        if (mk >> (8 + m) & 1u) acc[2] += rho;
       }
       // z-edge points: for margin <= T only the first and last of a thread's
       // points can be within margin of a z face
@@ -165,18 +165,22 @@ __device__ __forceinline__ void z_observe(const ZArgs& a, const CV* v, int t, ui
     }
     if (line_edge) acc[3] = acc[0];  // every point of the line: the same sum in the same order
   }
-#pragma unroll
-  for (int k = 0; k < kObsVals; ++k) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-  }
+  // warp sums of the four values by a transposing tree: the first level
+  // trades half of the values between the half-warps, the second half of the
+  // rest between quarter-warps, so 12 shuffles and 6 additions instead of
+  // 4 x 5 x 2 and 20 (the pass is bound by the L1 data pipe, which the
+  // shuffles share); lane 8 k ends with value k
   const int lane = threadIdx.x & 31;
-  if (lane < kObsVals) {
-    double r = acc[0];
+  const bool h16 = lane & 16, h8 = lane & 8;
+  const double k0 = h16 ? acc[2] : acc[0], k1 = h16 ? acc[3] : acc[1];
+  const double s0 = h16 ? acc[0] : acc[2], s1 = h16 ? acc[1] : acc[3];
+  const double b0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+  const double b1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+  double r = (h8 ? b1 : b0) + __shfl_xor_sync(0xffffffffu, h8 ? b0 : b1, 8);
 #pragma unroll
-    for (int k = 1; k < kObsVals; ++k) r = lane == k ? acc[k] : r;
-    a.obs_partial[((size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kObsVals + lane] = r;
-  }
+  for (int o = 4; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  if ((lane & 7) == 0)
+    a.obs_partial[((size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kObsVals + (lane >> 3)] = r;
 }
 
 template <int L, int KIND, bool VTAB, typename CV, int CH = 0, bool OBS = false>
@@ -495,12 +499,45 @@ int64_t ctap_z_blocks(const ctap_plan* p) {
   return (nlines + C - 1) / C * ((threads + 31) / 32);
 }
 
+// The guide-partition bits of z_observe for lines of length L (T = L/8
+// threads per line): the comparisons of observables.py:96-99 (xs[x] < xb1[z],
+// xs[x] >= xb2[z]) evaluated once per (x, t) for the thread's 8 points.
+template <int L>
+__global__ void obs_mask_kernel(const double* __restrict__ xs, const double* __restrict__ xb1,
+                                const double* __restrict__ xb2, uint32_t nx, uint16_t* __restrict__ mask) {
+  constexpr int T = L / kElems;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nx * T) return;
+  const uint32_t x = i / T, t = i % T;
+  const double xv = xs[x];
+  uint32_t mk = 0;
+#pragma unroll
+  for (int m = 0; m < kElems; ++m) {
+    const int z = t + m * T;
+    if (xv < xb1[z]) mk |= 1u << m;
+    if (xv >= xb2[z]) mk |= 1u << (8 + m);
+  }
+  mask[i] = (uint16_t)mk;
+}
+
+// u16 entries of the partition mask of a plan's fused observer pass
+size_t ctap_obs_mask_entries(const ctap_plan* p) { return (size_t)p->n[0] * (p->n[2] / kElems); }
+
 // [z^-1 . Vh] with the observer sums fused (single-GPU plans): block partials
 // of [sum rho, left, middle, right, edge(margin)] into `partial`
 // (ctap_z_blocks(p) x 5 doubles)
 cudaError_t ctap_run_z_last_observe(const ctap_plan* p, void* psi, const double* xs, const double* xb1,
-                                    const double* xb2, int margin, double* partial, cudaStream_t st) {
+                                    const double* xb2, int margin, double* partial, uint16_t* mask,
+                                    cudaStream_t st) {
   const int64_t nz = p->n[2];
+  if (xb1) {
+    const uint32_t n = (uint32_t)ctap_obs_mask_entries(p);
+#define CTAP_OM(LL) (obs_mask_kernel<LL><<<(n + 255) / 256, 256, 0, st>>>(xs, xb1, xb2, (uint32_t)p->n[0], mask), \
+                     cudaGetLastError())
+    const cudaError_t e = [&]() -> cudaError_t { CTAP_BY_LENGTH(nz, CTAP_OM) }();
+#undef CTAP_OM
+    if (e != cudaSuccess) return e;
+  }
   ZArgs a{};
   a.psi = psi;
   a.out = psi;
@@ -511,6 +548,7 @@ cudaError_t ctap_run_z_last_observe(const ctap_plan* p, void* psi, const double*
   a.xb1 = xb1;
   a.xb2 = xb2;
   a.obs_partial = partial;
+  a.obs_mask = xb1 ? mask : nullptr;
   a.ny = (uint32_t)p->n[1];
   a.lny = (uint32_t)ilog2(p->n[1]);
   a.nx = (uint32_t)p->n[0];

@@ -46,6 +46,10 @@ struct ZArgs {
   const double* xb1;   // guide boundaries per z (null: no partition)
   const double* xb2;
   double* obs_partial;
+  // per (x, thread t of a line): bit m = xs[x] < xb1[t + m T], bit 8 + m =
+  // xs[x] >= xb2[t + m T] (obs_mask_kernel; one load per thread and line
+  // instead of two boundary loads per point)
+  const uint16_t* obs_mask;
   uint32_t ny, nx;     // line = x ny + y
   uint32_t lny;        // log2(ny)
   int margin;
