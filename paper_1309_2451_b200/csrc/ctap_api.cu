@@ -271,6 +271,10 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
     if (p->kin_stream[i]) cudaStreamDestroy(p->kin_stream[i]);
   for (int i = 0; i < 3; ++i)
     if (p->kin_ev[i]) cudaEventDestroy(p->kin_ev[i]);
+  for (int i = 0; i < 4; ++i)
+    if (p->pb_stream[i]) cudaStreamDestroy(p->pb_stream[i]);
+  for (int i = 0; i < 5; ++i)
+    if (p->pb_ev[i]) cudaEventDestroy(p->pb_ev[i]);
   delete p;
   return CTAP_OK;
 }
@@ -360,6 +364,115 @@ static cudaError_t kin_block(ctap_plan* p, void* psi, cudaStream_t st) {
   return e;
 }
 
+// Position block by x-slabs: the passes between two x passes, [y^-1,
+// z^-1 V z, y], are independent per x-plane, so each slab of x-planes runs
+// its three passes back to back -- its psi and v_i stay in L2 between them --
+// with consecutive slabs on kPBStreams streams (forked from and joined back
+// into the caller's stream; graph branches under capture).  Slab size: three
+// slabs' psi + v_i within ~80 MB of the 126 MB L2 (4 planes at 512^3); off
+// when psi + v_i fit L2 anyway (launch-bound small grids).  CTAP_PBLOCK
+// overrides (0 off, k planes).  Bitwise equal to the plane-order schedule:
+// every pass computes each line and tile exactly as before.
+constexpr int kPBStreams = 3;
+static int64_t pblock_planes(const ctap_plan* p) {
+  static const int64_t env = [] {
+    const char* e = getenv("CTAP_PBLOCK");
+    return e ? (int64_t)atoll(e) : (int64_t)-1;
+  }();
+  // (1024-point y lines run on the persistent ring, which a few-plane slab
+  // starves: 1024^2 x 512 measured 18.3 -> 21.4 ms per step)
+  if (p->expv_dev || p->kbuf || p->zchunk || p->z2 || p->slab_p != 1 || p->n[1] > 512) return 0;
+  const size_t csz = p->dtype == CTAP_C64 ? 8 : 16;
+  const double plane = (double)p->n[1] * p->n[2] * (csz + sizeof(double));
+  int64_t v = env;
+  if (v < 0) {
+    if (plane * p->nx_local <= 126e6) return 0;
+    v = 1;
+    while (2 * v * plane * kPBStreams <= 80e6) v *= 2;
+  }
+  if (v <= 0 || v >= p->nx_local || p->nx_local % v) return 0;
+  return v;
+}
+static int pblock_streams() {
+  static const int v = [] {
+    const char* e = getenv("CTAP_PBLOCK_STREAMS");
+    return e ? atoi(e) : kPBStreams;
+  }();
+  return v < 1 ? 1 : v > 4 ? 4 : v;
+}
+// phase 1: slab's [z V_h] [y]; 0: [y^-1] [z^-1 V z] [y]; 2: [y^-1] [z^-1 V_h]
+// (3: [y^-1] only, the observed segment end)
+static cudaError_t pblock_triples(ctap_plan* p, void* psi, int phase, cudaStream_t st) {
+  const int64_t planes = pblock_planes(p), ny = p->n[1], nz = p->n[2];
+  const size_t csz = p->dtype == CTAP_C64 ? 8 : 16;
+  const int ns = pblock_streams();
+  cudaError_t e = cudaSuccess;
+  if (ns > 1) {
+    for (int i = 0; i < ns && e == cudaSuccess; ++i)
+      if (!p->pb_stream[i]) e = cudaStreamCreateWithFlags(&p->pb_stream[i], cudaStreamNonBlocking);
+    for (int i = 0; i <= ns && e == cudaSuccess; ++i)
+      if (!p->pb_ev[i]) e = cudaEventCreateWithFlags(&p->pb_ev[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(p->pb_ev[0], st);
+    for (int i = 0; i < ns && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(p->pb_stream[i], p->pb_ev[0], 0);
+  }
+  for (int64_t x0 = 0, c = 0; x0 < p->nx_local && e == cudaSuccess; x0 += planes, ++c) {
+    cudaStream_t s = ns > 1 ? p->pb_stream[c % ns] : st;
+    ctap_plan t = *p;
+    t.nx_local = planes;
+    t.n[0] = planes;  // the y pass sizes its grid by n[0] / slab_p
+    t.vi_dev = p->vi_dev + x0 * ny * nz;
+    void* ps = (char*)psi + csz * (size_t)(x0 * ny * nz);
+    if (phase != 1) e = ctap_run_pass(&t, CTAP_PASS_Y_INV, ps, ps, s);
+    if (phase != 3) {
+      if (e == cudaSuccess)
+        e = ctap_run_pass(&t, phase == 1 ? CTAP_PASS_Z_FIRST : phase == 0 ? CTAP_PASS_Z_MID : CTAP_PASS_Z_LAST, ps,
+                          ps, s);
+      if (e == cudaSuccess && phase != 2) e = ctap_run_pass(&t, CTAP_PASS_Y_FWD, ps, ps, s);
+    }
+  }
+  if (ns > 1)
+    for (int i = 0; i < ns && e == cudaSuccess; ++i) {
+      e = cudaEventRecord(p->pb_ev[1 + i], p->pb_stream[i]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, p->pb_ev[1 + i], 0);
+    }
+  return e;
+}
+
+static int advance_pblock(ctap_plan* p, void* psi, int64_t n, cudaStream_t st) {
+  CUDA_TRY(pblock_triples(p, psi, 1, st), "ctap_advance");
+  int64_t j = 0;
+  if (graphs_enabled() && n - 1 >= kGraphSteps) {
+    if (p->g_exec == nullptr || p->g_psi != psi || p->g_steps != kGraphSteps) {
+      if (p->g_exec) cudaGraphExecDestroy(p->g_exec);
+      p->g_exec = nullptr;
+      if (!p->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking), "ctap_advance");
+      cudaGraph_t g = nullptr;
+      CUDA_TRY(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal), "ctap_advance capture");
+      cudaError_t ce = cudaSuccess;
+      for (int m = 0; m < kGraphSteps && ce == cudaSuccess; ++m) {
+        ce = ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, p->cap_stream);
+        if (ce == cudaSuccess) ce = pblock_triples(p, psi, 0, p->cap_stream);
+      }
+      cudaError_t ee = cudaStreamEndCapture(p->cap_stream, &g);
+      if (ce == cudaSuccess) ce = ee;
+      if (ce == cudaSuccess) ce = cudaGraphInstantiate(&p->g_exec, g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (ce != cudaSuccess) {
+        p->g_exec = nullptr;
+        return cuda_fail(ce, "ctap_advance graph capture");
+      }
+      p->g_psi = psi;
+      p->g_steps = kGraphSteps;
+    }
+    for (; j + kGraphSteps <= n - 1; j += kGraphSteps) CUDA_TRY(cudaGraphLaunch(p->g_exec, st), "ctap_advance");
+  }
+  for (; j < n; ++j) {
+    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, st), "ctap_advance");
+    CUDA_TRY(pblock_triples(p, psi, j < n - 1 ? 0 : p->skip_last ? 3 : 2, st), "ctap_advance");
+  }
+  return CTAP_OK;
+}
+
 CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
   Range nvtx("ctap_advance %lld steps", (long long)n);
   if (!p || !psi) return fail(CTAP_EINVAL, "null argument");
@@ -368,6 +481,7 @@ CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
   if (!p->vi_dev) return fail(CTAP_EINVAL, "plan has no potential");
   if (n == 0) return CTAP_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  if (pblock_planes(p)) return advance_pblock(p, psi, n, st);
   CUDA_TRY(ctap_run_pass(p, CTAP_PASS_Z_FIRST, psi, psi, st), "ctap_advance");
   // interior steps in CUDA-graph chunks: one launch per kGraphSteps steps
   // instead of 4 (removes the per-kernel launch cost that dominates small grids)

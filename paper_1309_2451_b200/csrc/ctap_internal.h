@@ -90,6 +90,8 @@ struct ctap_plan {
   cudaStream_t cap_stream;
   cudaStream_t kin_stream[2];  // z-chunked kinetic block: two concurrent chunk pipelines
   cudaEvent_t kin_ev[3];
+  cudaStream_t pb_stream[4];   // x-slab position blocks (ctap_advance)
+  cudaEvent_t pb_ev[5];
   cudaGraphExec_t g_exec;
   const void* g_psi;
   int g_steps;

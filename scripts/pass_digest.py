@@ -1,6 +1,6 @@
 """Bitwise digest of one pass on a seeded random psi (A/B of kernel variants).
 
-usage: python scripts/pass_digest.py NX NY NZ PASS [PASS ...]
+usage: python scripts/pass_digest.py NX NY NZ PASS [PASS ...]   (PASS: a pass name or ADVANCE<n>)
 Prints, per pass name (pass_timing.py's names), an int64 sum of the output's
 bit patterns: two kernels are bitwise interchangeable iff their digests match.
 """
@@ -28,7 +28,10 @@ def main():
     gen = torch.Generator(device="cuda").manual_seed(7)
     for name in sys.argv[4:]:
         psi = torch.randn(nx, ny, nz, dtype=torch.complex128, device="cuda", generator=gen) * 1e-3
-        plan.native.run_pass(getattr(_lib, "PASS_" + name), psi, psi)
+        if name.startswith("ADVANCE"):
+            plan.native.advance(psi, int(name[7:] or 20))
+        else:
+            plan.native.run_pass(getattr(_lib, "PASS_" + name), psi, psi)
         torch.cuda.synchronize()
         d = int(torch.view_as_real(psi).contiguous().view(torch.int64).sum().item())
         print(f"{name} digest {d}")

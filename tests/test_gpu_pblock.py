@@ -1,0 +1,35 @@
+"""The x-slab position-block schedule of ctap_advance (the passes between
+two x passes, [y^-1, z^-1 V z, y], run slab by slab on three streams so a
+slab stays in L2) is bitwise equal to the plane-order schedule: psi and every
+trace row of an observed evolve_real, eager steps, graph-captured steps and
+the fused observer segment end included.  The schedule is chosen from
+CTAP_PBLOCK when the plan is made, so each variant runs in its own process."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _digest(env_extra, n=256, steps=45, stride=20):
+    env = dict(os.environ, **env_extra)
+    out = subprocess.run([sys.executable, os.path.join(HERE, "schedule_digest.py"), str(n), str(steps), str(stride)],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="no CUDA device")
+def test_position_block_schedule_bitwise_equal():
+    ref = _digest({"CTAP_PBLOCK": "0"})
+    assert len(ref["rows"]) == 4  # t = 0, 20, 40 and the final step; 20-step segments use the step graphs
+    for planes, streams in (("16", "3"), ("8", "1"), ("32", "2")):
+        got = _digest({"CTAP_PBLOCK": planes, "CTAP_PBLOCK_STREAMS": streams})
+        assert got == ref, (planes, streams)
