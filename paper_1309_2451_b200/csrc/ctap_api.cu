@@ -275,6 +275,8 @@ CTAP_API int ctap_plan_destroy(ctap_plan* p) {
     if (p->pb_stream[i]) cudaStreamDestroy(p->pb_stream[i]);
   for (int i = 0; i < 5; ++i)
     if (p->pb_ev[i]) cudaEventDestroy(p->pb_ev[i]);
+  for (auto g : p->pb_exec)
+    if (g) cudaGraphExecDestroy(g);
   delete p;
   return CTAP_OK;
 }
@@ -438,8 +440,47 @@ static cudaError_t pblock_triples(ctap_plan* p, void* psi, int phase, cudaStream
   return e;
 }
 
+// One piece of the slab schedule: the segment start (phase 1: the slab
+// triples alone) or an x pass followed by the triples of phase 0 / 2 / 3.
+static cudaError_t pblock_piece(ctap_plan* p, void* psi, int phase, cudaStream_t s) {
+  cudaError_t e = phase == 1 ? cudaSuccess : ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, s);
+  return e == cudaSuccess ? pblock_triples(p, psi, phase, s) : e;
+}
+
+// The same as a graph (hundreds of small launches), captured once per psi
+// pointer and phase and replayed on st.
+static cudaError_t pblock_graph(ctap_plan* p, void* psi, int phase, cudaStream_t st) {
+  if (!graphs_enabled()) return pblock_piece(p, psi, phase, st);
+  if (p->pb_psi != psi) {
+    for (auto& g : p->pb_exec)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+    p->pb_psi = psi;
+  }
+  cudaGraphExec_t& ex = p->pb_exec[phase];
+  if (!ex) {
+    cudaError_t e = cudaSuccess;
+    if (!p->cap_stream) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return e;
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = pblock_piece(p, psi, phase, p->cap_stream);
+    cudaError_t ee = cudaStreamEndCapture(p->cap_stream, &g);
+    if (ce == cudaSuccess) ce = ee;
+    if (ce == cudaSuccess) ce = cudaGraphInstantiate(&ex, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (ce != cudaSuccess) {
+      ex = nullptr;
+      return ce;
+    }
+  }
+  return cudaGraphLaunch(ex, st);
+}
+
 static int advance_pblock(ctap_plan* p, void* psi, int64_t n, cudaStream_t st) {
-  CUDA_TRY(pblock_triples(p, psi, 1, st), "ctap_advance");
+  CUDA_TRY(pblock_graph(p, psi, 1, st), "ctap_advance");
   int64_t j = 0;
   if (graphs_enabled() && n - 1 >= kGraphSteps) {
     if (p->g_exec == nullptr || p->g_psi != psi || p->g_steps != kGraphSteps) {
@@ -467,8 +508,7 @@ static int advance_pblock(ctap_plan* p, void* psi, int64_t n, cudaStream_t st) {
     for (; j + kGraphSteps <= n - 1; j += kGraphSteps) CUDA_TRY(cudaGraphLaunch(p->g_exec, st), "ctap_advance");
   }
   for (; j < n; ++j) {
-    CUDA_TRY(ctap_run_pass(p, CTAP_PASS_X_KIN, psi, psi, st), "ctap_advance");
-    CUDA_TRY(pblock_triples(p, psi, j < n - 1 ? 0 : p->skip_last ? 3 : 2, st), "ctap_advance");
+    CUDA_TRY(pblock_graph(p, psi, j < n - 1 ? 0 : p->skip_last ? 3 : 2, st), "ctap_advance");
   }
   return CTAP_OK;
 }

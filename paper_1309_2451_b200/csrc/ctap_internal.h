@@ -92,6 +92,8 @@ struct ctap_plan {
   cudaEvent_t kin_ev[3];
   cudaStream_t pb_stream[4];   // x-slab position blocks (ctap_advance)
   cudaEvent_t pb_ev[5];
+  cudaGraphExec_t pb_exec[4];  // their pieces as graphs, by phase (0 step, 1 segment start, 2/3 ends) for pb_psi
+  const void* pb_psi;
   cudaGraphExec_t g_exec;
   const void* g_psi;
   int g_steps;
