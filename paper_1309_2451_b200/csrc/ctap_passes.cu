@@ -837,6 +837,7 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
     case PASS_WY_FWD: {  // diagnostics: the warp-per-line TMA pipeline on x / y lines
       if (in != out) return cudaErrorInvalidValue;
       const bool xa = kind == PASS_WX_COPY;
+      a.lin = a.lout = xa ? x_nat : y_nat;
       a.n_outer = xa ? nyl : nxl;
       a.ph.outer_off = xa ? (uint32_t)p->slab_r * nyl : 0u;
       return ctap_run_wline(p, xa ? 2 : 1, kind == PASS_WY_FWD ? T_FWD : T_COPY, p->wline == 2 ? 2 : 1, out, a, st);
@@ -859,10 +860,10 @@ cudaError_t ctap_run_pass_z(const ctap_plan* p, int kind, const void* in, void* 
       a.ph.outer_off = (uint32_t)p->slab_r * nyl;
       const Tw tw = twid(p, nx);
       const int L = (int)nx;
-      if (kind == PASS_X_KIN && !c64 && !zsub && in == out && !p->expk_dev) {
+      if (kind == PASS_X_KIN && !c64 && (!zsub || nx <= 512) && in == out && !p->expk_dev) {
         // warp-per-line TMA pipeline (ctap_wline.cu): the default complex128 x pass
         const int tk = kind == PASS_X_KIN ? T_KIN : kind == PASS_X_FWD ? T_FWD : T_INV;
-        cudaError_t e = ctap_run_wline(p, 2, tk, p->wline, out, a, st);
+        cudaError_t e = ctap_run_wline(p, 2, tk, p->wline, a.out, a, st);  // a.out: offset to the z chunk
         if (e != cudaErrorNotSupported) return e;
       }
       if (use_tma_x && in == out && !(kind == PASS_X_KIN && p->expk_dev)) {

@@ -520,12 +520,16 @@ static cudaError_t launch_ring(const TileArgs& a, void* data, const double2* tw,
   if (L >= 1024) wpc = 2;
   EncodeTiledFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
-  const uint64_t nz2 = (uint64_t)a.nchunk * W * 2;  // scalars per z line
+  const uint64_t nz2 = (uint64_t)a.nchunk * W * 2;  // scalars of the pass's z columns
+  // z pitch of the array in scalars: the x pass of a z chunk (a.in offset
+  // by z0) covers nz2 of them
+  const uint64_t pitch2 = (uint64_t)(AXIS == 2 ? a.lin.so : a.lin.si) * 2;
+  if (pitch2 < nz2) return cudaErrorInvalidValue;
   const uint64_t d1 = AXIS == 2 ? a.n_outer : L, d2 = AXIS == 2 ? L : a.n_outer;
   CUtensorMap map;
   std::memset(&map, 0, sizeof map);
   const cuuint64_t dims[3] = {nz2, d1, d2};
-  const cuuint64_t strides[2] = {nz2 * sizeof(double), nz2 * sizeof(double) * d1};
+  const cuuint64_t strides[2] = {pitch2 * sizeof(double), pitch2 * sizeof(double) * d1};
   const cuuint32_t box[3] = {2 * W, AXIS == 2 ? 1u : (cuuint32_t)BOX, AXIS == 2 ? (cuuint32_t)BOX : 1u};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, data, dims, strides, box, estr,
