@@ -381,14 +381,16 @@ static int64_t pblock_planes(const ctap_plan* p) {
     const char* e = getenv("CTAP_PBLOCK");
     return e ? (int64_t)atoll(e) : (int64_t)-1;
   }();
-  // (1024-point y lines run on the persistent ring, which a few-plane slab
-  // starves: 1024^2 x 512 measured 18.3 -> 21.4 ms per step)
-  if (p->expv_dev || p->kbuf || p->zchunk || p->z2 || p->slab_p != 1 || p->n[1] > 512) return 0;
+  if (p->expv_dev || p->kbuf || p->zchunk || p->z2 || p->slab_p != 1) return 0;
   const size_t csz = p->dtype == CTAP_C64 ? 8 : 16;
   const double plane = (double)p->n[1] * p->n[2] * (csz + sizeof(double));
   int64_t v = env;
   if (v < 0) {
-    if (plane * p->nx_local <= 126e6) return 0;
+    // automatic for complex128 with y lines <= 512 points: the 1024-point y
+    // ring and complex64's TMA y passes are persistent kernels that a
+    // few-plane slab starves (1024^2 x 512: 18.3 -> 21.4 ms per step;
+    // complex64 512^3: 2.82 -> 3.45 ms)
+    if (p->dtype != CTAP_C128 || p->n[1] > 512 || plane * p->nx_local <= 126e6) return 0;
     v = 1;
     while (2 * v * plane * kPBStreams <= 80e6) v *= 2;
   }
