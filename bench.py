@@ -449,6 +449,9 @@ def run_ours(args):
             "data": "synthetic: paper-chip CTAP potential (device Biot-Savart, 9605 segments) and a Gaussian packet",
             "config": _config(n),
             "details": {"decomposition": decomp or "single GPU",
+                        "step_schedule": ("x-slab position blocks: %d planes on %d streams" % prop.native.step_schedule()
+                                          if isinstance(prop, _Single) and prop.native.step_schedule()[0]
+                                          else "plane order"),
                         "phase_factors": "both on the fly (exact recipe)",
                         "bytes_per_point_step": BYTES_PER_POINT_STEP, "l2": l2_note},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": dom["gbs"], "peak": peak,
@@ -467,7 +470,7 @@ def run_ours(args):
             "per_pass_ms": {k: round(v["ms"], 4) for k, v in per_pass.items()},
             "observer_event": obs_cost,
             "clocks": clk.summary(),
-            "gpu_launches": 4 * args.steps + 1,
+            "gpu_launches": prop.native.launches(args.steps) if isinstance(prop, _Single) else 4 * args.steps + 1,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "setup": {"potential_seconds": t_pot, "norm_after": norm, "wall_seconds_timed": wall},

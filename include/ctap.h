@@ -140,6 +140,13 @@ CTAP_API int ctap_plan_destroy(ctap_plan* plan);
  * n_steps == 0 leaves psi untouched. */
 CTAP_API int ctap_advance(ctap_plan* plan, void* psi_dev, int64_t n_steps, void* stream);
 
+/* The step schedule ctap_advance uses for this plan (no reference
+ * counterpart: introspection for benchmarks and tests).  *slab_planes = 0:
+ * plane order, 4 launches per step; k > 0: x-slab position blocks of k
+ * planes on *streams streams, the passes [y^-1] [z^-1 V z] [y] of each slab
+ * run back to back between the x passes (1 + 3 nx/k launches per step). */
+CTAP_API int ctap_step_schedule(const ctap_plan* plan, int64_t* slab_planes, int32_t* streams);
+
 /* evolve_real's segment + observer event (propagator.py:160-168): n telescoped
  * steps, then the raw sums of ctap_observe ([sum rho, left, middle, right,
  * edge(margin)] into out_dev[5]) -- computed inside the segment-end pass

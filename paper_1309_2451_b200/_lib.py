@@ -39,7 +39,7 @@ EXPORTS = (
     "ctap_density_xz", "ctap_k2_sums", "ctap_v_sums", "ctap_v_sums_with", "ctap_phase_field", "ctap_scale",
     "ctap_fft3d", "ctap_potential", "ctap_last_error", "ctap_version",
     "ctap_set_peer_buffers", "ctap_ipc_handle", "ctap_ipc_open", "ctap_ipc_close",
-    "ctap_device_alloc", "ctap_device_free", "ctap_slice_minima", "ctap_flag_barrier",
+    "ctap_device_alloc", "ctap_device_free", "ctap_slice_minima", "ctap_flag_barrier", "ctap_step_schedule",
 )
 
 
@@ -101,6 +101,7 @@ def load():
         "ctap_device_free": [p],
         "ctap_slice_minima": [p, i64, i64, i64, p, p, p],
         "ctap_flag_barrier": [ctypes.POINTER(p), p, i32, i32, ctypes.c_uint32, p],
+        "ctap_step_schedule": [p, ctypes.POINTER(i64), ctypes.POINTER(i32)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

@@ -515,6 +515,13 @@ static int advance_pblock(ctap_plan* p, void* psi, int64_t n, cudaStream_t st) {
   return CTAP_OK;
 }
 
+CTAP_API int ctap_step_schedule(const ctap_plan* p, int64_t* slab_planes, int32_t* streams) {
+  if (!p || !slab_planes || !streams) return fail(CTAP_EINVAL, "null argument");
+  *slab_planes = pblock_planes(p);
+  *streams = *slab_planes ? pblock_streams() : 1;
+  return CTAP_OK;
+}
+
 CTAP_API int ctap_advance(ctap_plan* p, void* psi, int64_t n, void* stream) {
   Range nvtx("ctap_advance %lld steps", (long long)n);
   if (!p || !psi) return fail(CTAP_EINVAL, "null argument");

@@ -96,6 +96,23 @@ class NativePlan:
     def advance(self, psi: torch.Tensor, n: int):
         _lib.call("ctap_advance", self.handle, psi.data_ptr(), int(n), _device.stream_handle())
 
+    def step_schedule(self) -> tuple[int, int]:
+        """(slab planes, streams) of ctap_advance's step schedule; (0, 1) is
+        plane order (ctap_step_schedule)."""
+        planes, streams = ctypes.c_int64(), ctypes.c_int32()
+        _lib.call("ctap_step_schedule", self.handle, ctypes.byref(planes), ctypes.byref(streams))
+        return planes.value, streams.value
+
+    def launches(self, n: int) -> int:
+        """Kernel launches of ctap_advance(n) under its step schedule."""
+        if n <= 0:
+            return 0
+        planes, _ = self.step_schedule()
+        if planes == 0:
+            return 4 * n + 1
+        s = self.grid.n[0] // planes
+        return 2 * s + (n - 1) * (1 + 3 * s) + 1 + 2 * s
+
     def advance_observe(self, psi: torch.Tensor, n: int, xs: torch.Tensor, xb1, xb2, margin: int) -> torch.Tensor:
         """n steps, then the observer sums fused into the segment-end pass
         (ctap_advance_observe): [sum rho, left, middle, right, edge]."""

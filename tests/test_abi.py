@@ -77,3 +77,4 @@ def test_null_arguments_rejected():
     assert lib.ctap_observe(None, None, None, None, None, 2, None, None) == _lib.CTAP_EINVAL
     assert lib.ctap_potential(None, 1, None, 1, None, 1, None, None, None, 0,
                               0., 0., 0., 0., 0., 0., 0., 0., None, None) == _lib.CTAP_EINVAL
+    assert lib.ctap_step_schedule(None, None, None) == _lib.CTAP_EINVAL

@@ -36,3 +36,23 @@ def test_position_block_schedule_bitwise_equal(precision):
     for planes, streams in variants:
         got = _digest({"CTAP_PBLOCK": planes, "CTAP_PBLOCK_STREAMS": streams}, precision)
         assert got == ref, (planes, streams)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="no CUDA device")
+def test_schedule_choice_and_launch_count():
+    """ctap_step_schedule reports the automatic choice: x-slabs for a
+    complex128 grid whose psi + v_i exceed the L2 (4 planes at 512^3 on
+    three streams, 16 at 256^3), plane order for complex64 and small grids."""
+    import numpy as np
+
+    from paper_1309_2451_b200 import propagator, qgrid
+
+    if os.environ.get("CTAP_PBLOCK"):
+        pytest.skip("CTAP_PBLOCK overrides the automatic choice")
+    for n, precision, want in ((256, "complex128", (16, 3)), (256, "complex64", (0, 1)), (64, "complex128", (0, 1))):
+        grid = qgrid.make_grid(n, n, n, (20e-6, 4e-6, 1000e-6))
+        plan = propagator.make_plan(grid, np.zeros(grid.n), 1.0e-26, 1e-6, precision=precision)
+        assert plan.native.step_schedule() == want, (n, precision)
+        planes = want[0]
+        assert plan.native.launches(20) == (4 * 20 + 1 if planes == 0 else
+                                            2 * (n // planes) + 19 * (1 + 3 * (n // planes)) + 1 + 2 * (n // planes))
