@@ -381,7 +381,7 @@ static int64_t pblock_planes(const ctap_plan* p) {
     const char* e = getenv("CTAP_PBLOCK");
     return e ? (int64_t)atoll(e) : (int64_t)-1;
   }();
-  if (p->expv_dev || p->kbuf || p->zchunk || p->z2 || p->slab_p != 1) return 0;
+  if (p->kbuf || p->zchunk || p->z2 || p->slab_p != 1) return 0;
   const size_t csz = p->dtype == CTAP_C64 ? 8 : 16;
   const double plane = (double)p->n[1] * p->n[2] * (csz + sizeof(double));
   int64_t v = env;
@@ -425,6 +425,7 @@ static cudaError_t pblock_triples(ctap_plan* p, void* psi, int phase, cudaStream
     t.nx_local = planes;
     t.n[0] = planes;  // the y pass sizes its grid by n[0] / slab_p
     t.vi_dev = p->vi_dev + x0 * ny * nz;
+    if (p->expv_dev) t.expv_dev = (char*)p->expv_dev + csz * (size_t)(x0 * ny * nz);
     void* ps = (char*)psi + csz * (size_t)(x0 * ny * nz);
     if (phase != 1) e = ctap_run_pass(&t, CTAP_PASS_Y_INV, ps, ps, s);
     if (phase != 3) {
