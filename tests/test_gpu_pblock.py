@@ -36,6 +36,11 @@ def test_position_block_schedule_bitwise_equal(precision):
     for planes, streams in variants:
         got = _digest({"CTAP_PBLOCK": planes, "CTAP_PBLOCK_STREAMS": streams}, precision)
         assert got == ref, (planes, streams)
+    if precision == "complex128":
+        # with the exp(-iV dt) plan table (offset per slab like v_i); the table
+        # holds the on-the-fly recipe's factors, so psi is the same bit for bit
+        got = _digest({"CTAP_PBLOCK": "16", "CTAP_PHASE_TABLES": "1"}, precision)
+        assert got == ref
 
 
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="no CUDA device")
