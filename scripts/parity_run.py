@@ -7,7 +7,7 @@ cfg2b  128x128x256 Ioffe-floor harmonic (population-moving), 5000 steps / 25
 cfg2   128x128x256 scaled-chip CTAP (configs/scaled.cfg with n_y = 128),
        25,000 steps, PopulationRecorder every 50 (V checked on all points)
 cfg3   256^3 paper-chip CTAP, 1000 steps / 100
-cfg4   512^3 paper-chip CTAP, 100 steps / 50
+cfg4   512^3 paper-chip CTAP, 100 steps / 50 (cfg4long: 1000 steps, ~10 min of oracle)
 cfg3c64 / cfg4c64  the same in complex64 mode, gate 1e-4 against the oracle
 cfg5   1024x1024x512 harmonic trap, 5 steps (one GPU vs the oracle, ~50 GB host RAM)
 
@@ -35,6 +35,7 @@ CASES = {
     "cfg2": lambda: (bc.cfg2(every=None), 25000, "complex128"),
     "cfg3": lambda: (bc.cfg3(every=8), 1000, "complex128"),
     "cfg4": lambda: (bc.cfg4(every=8), 100, "complex128"),
+    "cfg4long": lambda: (bc.cfg4(every=16), 1000, "complex128"),
     "cfg3c64": lambda: (bc.cfg3(every=8), 1000, "complex64"),
     "cfg4c64": lambda: (bc.cfg4(every=8), 100, "complex64"),
     "cfg5": lambda: (bc.cfg5(), 5, "complex128"),
