@@ -419,8 +419,14 @@ static cudaError_t pblock_triples(ctap_plan* p, void* psi, int phase, cudaStream
     if (e == cudaSuccess) e = cudaEventRecord(p->pb_ev[0], st);
     for (int i = 0; i < ns && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(p->pb_stream[i], p->pb_ev[0], 0);
   }
+  static const int pdl = [] {
+    const char* v = getenv("CTAP_PDL");
+    return v ? atoi(v) : 1;
+  }();
   for (int64_t x0 = 0, c = 0; x0 < p->nx_local && e == cudaSuccess; x0 += planes, ++c) {
     cudaStream_t s = ns > 1 ? p->pb_stream[c % ns] : st;
+    // the first grid of each stream follows an event wait, not a grid
+    ctap_pdl = pdl && c >= ns;
     ctap_plan t = *p;
     t.nx_local = planes;
     t.n[0] = planes;  // the y pass sizes its grid by n[0] / slab_p
@@ -435,6 +441,7 @@ static cudaError_t pblock_triples(ctap_plan* p, void* psi, int phase, cudaStream
       if (e == cudaSuccess && phase != 2) e = ctap_run_pass(&t, CTAP_PASS_Y_FWD, ps, ps, s);
     }
   }
+  ctap_pdl = 0;
   if (ns > 1)
     for (int i = 0; i < ns && e == cudaSuccess; ++i) {
       e = cudaEventRecord(p->pb_ev[1 + i], p->pb_stream[i]);

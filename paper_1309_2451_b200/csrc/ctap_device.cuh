@@ -208,6 +208,11 @@ struct SmemStrided {  // column-fastest tile of W columns: element i of column c
   __device__ __forceinline__ C& at(int i) const { return base[i * W]; }
 };
 
+// Programmatic dependent launch (griddepcontrol): no-ops for grids launched
+// without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // Barrier among the threads that share one exchange buffer.
 struct SyncBlock {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }

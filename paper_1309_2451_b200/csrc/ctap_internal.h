@@ -112,6 +112,7 @@ struct ZArgs;
 int64_t ctap_z_blocks(const ctap_plan* p);
 cudaError_t ctap_run_pass_chunk(const ctap_plan* p, int kind, const void* in, void* out, int64_t z0, int64_t zn,
                                 cudaStream_t st);
+extern thread_local int ctap_pdl;  // launch the z / y pass kernels with programmatic dependent launch
 size_t ctap_obs_mask_entries(const ctap_plan* p);
 cudaError_t ctap_run_z_last_observe(const ctap_plan* p, void* psi, const double* xs, const double* xb1,
                                     const double* xb2, int margin, double* partial, uint16_t* mask,

@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::
   // element z of this line: natural off + z, or z-chunked (pencil)
   const uint32_t zmask = (1u << a.lzc) - 1u, coff = line << a.lzc;
   auto at_in = [&](uint32_t zz) { return CH & 1 ? (zz >> a.lzc) * a.cs + coff + (zz & zmask) : off + zz; };
+  pdl_wait();  // programmatic dependent launch: the preceding grid's stores are visible from here
   auto at_out = [&](uint32_t zz) { return CH & 2 ? (zz >> a.lzc) * a.cs + coff + (zz & zmask) : off + zz; };
   SmemContig<CV> sm{smem + c * Cfg::smem_line};
   CV v[kElems];
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(ZCfg<L, CV>::threads, ZMinBlocks<KIND, VTAB>::
   } else {
     z_body<L, KIND, VTAB>(a, v, t, off, active, tw, sm, SyncNamed{1 + c, Cfg::T});
   }
+  pdl_trigger();  // the next grid of the stream may start its launch (it waits for our stores)
   if (active) {
 #pragma unroll
     for (int m = 0; m < kElems; ++m) __stcg(&psi[at_out(t + m * Cfg::T)], v[m]);
@@ -261,9 +263,11 @@ __global__ void __launch_bounds__(TileCfg<L, CV, W>::threads,
   constexpr int E = Cfg::E;
   const uint32_t obi = outer(a.lin, o) + z, obo = outer(a.lout, o) + z;
   CV v[E];
+  pdl_wait();
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = active ? in[obi + inner<PIN>(a.lin, t + m * Cfg::T)] : CT<CV>::mk(0, 0);
   tile_body<L, E, KIND, KTAB, POUT>(a, v, t, o, z, active, tw, SmemStrided<CV, W>{smem + (size_t)g * L * W + col});
+  pdl_trigger();
   if (active) {
     if constexpr (PEERS) {
       // fused transpose: each point goes straight into the owning rank's
@@ -289,14 +293,39 @@ __global__ void __launch_bounds__(TileCfg<L, CV, W>::threads,
 // ---------------------------------------------------------------------------
 
 
+// Launch through cudaLaunchKernelEx with programmatic stream serialization
+// while ctap_pdl is set (the x-slab schedule's chains of small per-slab
+// grids: the next grid's launch overlaps this one's tail; every kernel
+// launched this way starts with griddepcontrol.wait), else <<<>>>.
+}  // namespace ctap
+thread_local int ctap_pdl = 0;
+namespace ctap {
+template <typename K, typename... Args>
+static cudaError_t launch_pdl(K k, unsigned grid, unsigned block, size_t smem, cudaStream_t st, Args... args) {
+  if (!ctap_pdl) {
+    k<<<grid, block, smem, st>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 template <int L, int KIND, bool VTAB, typename CV, int CH = 0, bool OBS = false>
 static cudaError_t launch_z(const ZArgs& a, const TwOf<CV>* tw, cudaStream_t st) {
   using Cfg = ZCfg<L, CV>;
   auto k = zline_kernel<L, KIND, VTAB, CV, CH, OBS>;
   static std::atomic<uint64_t> attr_done{0};
   if (cudaError_t e = ctap_smem_attr(k, Cfg::smem, attr_done)) return e;
-  k<<<(a.nlines + Cfg::C - 1) / Cfg::C, Cfg::threads, Cfg::smem, st>>>(a, tw);
-  return cudaGetLastError();
+  return launch_pdl(k, (a.nlines + Cfg::C - 1) / Cfg::C, Cfg::threads, Cfg::smem, st, a, tw);
 }
 
 template <int L, int KIND, bool PIN, bool POUT, bool KTAB, typename CV, int W, bool PEERS = false>
@@ -306,8 +335,7 @@ static cudaError_t launch_tile(const TileArgs& a, const TwOf<CV>* tw, cudaStream
   static std::atomic<uint64_t> attr_done{0};
   if (cudaError_t e = ctap_smem_attr(k, Cfg::smem, attr_done)) return e;
   const uint32_t ntiles = a.n_outer * a.nchunk;
-  k<<<(ntiles + Cfg::G - 1) / Cfg::G, Cfg::threads, Cfg::smem, st>>>(a, tw);
-  return cudaGetLastError();
+  return launch_pdl(k, (ntiles + Cfg::G - 1) / Cfg::G, Cfg::threads, Cfg::smem, st, a, tw);
 }
 
 #define CTAP_BY_LENGTH(L, FN)                   \
