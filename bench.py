@@ -85,8 +85,11 @@ def _config(n):
     """The workload both arms report (identical dicts: the arms differ only in
     the implementation; decomposition etc. go to `details`)."""
     name = CONFIG_NAMES.get(tuple(n), "synthetic grid")
+    npts = int(n[0]) * int(n[1]) * int(n[2])
     return {"workload": f"{n[0]}x{n[1]}x{n[2]} CTAP split-step propagation, complex128, dt = 1 us, Li-6 ({name})",
-            "grid": list(n), "extents_m": list(EXTENTS)}
+            "grid": list(n), "extents_m": list(EXTENTS),
+            "l2": (f"inputs larger than L2 (psi + V = {24 * npts / 2**20:.0f} MiB > 126 MB), no flush"
+                   if 24 * npts > 126e6 else f"inputs {24 * npts / 2**20:.0f} MiB fit the 126 MB L2 (not flushed)")}
 
 
 # ---------------------------------------------------------------- clocks
