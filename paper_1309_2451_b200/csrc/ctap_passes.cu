@@ -105,11 +105,12 @@ __device__ __forceinline__ void z_body(const ZArgs& a, CV* v, int t, uint32_t of
   } else {  // T_VMID: inverse, V, forward; T_VLAST: inverse, Vh
     double vi[kElems];
     // v_i loaded before the inverse transform (its latency hides behind it),
-    // all but the last: holding all eight across the transform made ptxas
-    // spill at the 80-register budget (45 spill instructions vs 23), and the
-    // spill traffic shares the L1 pipe this kernel is bound by --
-    // [z^-1 V z] 1.08 -> 1.02 ms at 512^3 (8 / 7 / 6 / 5 early: 1.08 / 1.02 /
-    // 1.02 / 1.09; same-box A/B, bitwise identical results)
+    // all but the last: one register pair fewer held across the transform at
+    // the 80-register budget schedules it better -- [z^-1 V z] 1.08 -> 1.02
+    // ms at 512^3 (8 / 7 / 6 / 5 early: 1.08 / 1.02 / 1.02 / 1.09; same-box
+    // A/B, bitwise identical results).  (ptxas's spill count, 45 vs 23, is
+    // code around the never-taken |phi| >= 2^20 library sincos call: ncu
+    // counts no local load or store executed.)
 #ifndef CTAP_Z_VEARLY
 #define CTAP_Z_VEARLY 7
 #endif
